@@ -1,0 +1,541 @@
+#!/usr/bin/env python3
+"""Benchmark of the RISE/Shine sm100a back end (the BASELINE.json metric).
+
+One step = one execution of the hot path — the RISE program's kernel(s),
+emitted by `emit_cuda` from the ImperativeUnit the reference front end
+produces — over one batch of synthetic, seeded input already resident in
+HBM.  Default workload: BASELINE.json configs[1], gemv fp32 8192x8192
+(`mv.rise` + the toMapGlobal strategy).  Other configs: --workload.
+
+Prints ONE JSON line (rank 0).  Timing: W warm-up steps; K timed steps
+bracketed by barrier + synchronize; each step's kernels timed with CUDA
+events on the launching stream; L2 flushed (256 MiB write) between steps
+outside the events; max over ranks.  `e2e` repeats the step through the
+public host-buffer path (pinned H2D, launch, D2H).  `--impl reference`
+times the reference's own CPU implementation (its emitted C/OpenMP,
+oracle/_ref) on this host's cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))  # checker / CPU-baseline legs only
+
+L2_FLUSH_BYTES = 256 << 20
+FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # derived, BASELINE.md §2
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)",
+                "sm_max_mhz": d.get("sm_max_mhz", 1965.0)}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)", "sm_max_mhz": 1965.0}
+
+
+# ---------------------------------------------------------------------------
+# workloads: program, sizes, synthetic inputs, algorithmic work
+
+
+class Workload:
+    key = ""
+    config_index = 0
+
+    def __init__(self, rank=0, world=1):
+        self.rank, self.world = rank, world
+
+    def inputs(self):
+        raise NotImplementedError
+
+
+class Gemv(Workload):
+    key = "gemv"
+    program = "mv.rise + toMapGlobal strategy (BASELINE.md §4 C2)"
+    config_index = 2
+    n = m = 8192
+    metric_unit = "GB/s"
+    bound = "hbm"
+
+    def compile(self):
+        from paper_2201_03611_b200 import programs
+
+        return programs.compile_config(self.key), {"n": self.n, "m": self.m}
+
+    def inputs(self):
+        rng = np.random.default_rng(self.config_index + 1000 * self.rank)
+        M = rng.uniform(-1, 1, (self.n, self.m)).astype(np.float32)
+        x = rng.uniform(-1, 1, self.m).astype(np.float32)
+        return [M, x]
+
+    def work(self):  # algorithmic bytes per step (SURVEY.md §8 d)
+        return 4.0 * (self.n * self.m + self.m + self.n)
+
+    def cpu_sample(self, host):
+        import oracle
+
+        M, x = host
+        rows = self.n
+        t = _best_of(lambda: oracle.ref_mv(M[:rows], x), 3)
+        return {"value": self.work() / t / 1e9, "unit": "GB/s", "cores": oracle.threads(), "kind": "reference",
+                "sample": f"full {self.n}x{self.m} gemv, the reference's emitted OpenMP C (mv.rise + toMapGlobal, "
+                          f"oracle/_ref), best of 3"}
+
+
+class GemvOpt(Gemv):
+    key = "gemv_opt"
+    program = "mv.rise + the paper's Listing-3 strategy (mv_opt.elv), s = 32"
+
+    def compile(self):
+        from paper_2201_03611_b200 import programs
+
+        return programs.compile_config(self.key), {"n": self.n, "m": self.m, "s": 32}
+
+
+class Dot(Workload):
+    key = "dot"
+    program = "zip |> map(*) |> reduce(add) + fuseReduceMap;toReduceSeq (BASELINE.md §4 C1)"
+    config_index = 1
+    n = 1 << 24
+    metric_unit = "GB/s"
+    bound = "hbm"
+
+    def compile(self):
+        from paper_2201_03611_b200 import programs
+
+        return programs.compile_config(self.key), {"n": self.n}
+
+    def inputs(self):
+        rng = np.random.default_rng(self.config_index + 1000 * self.rank)
+        return [rng.uniform(-1, 1, self.n).astype(np.float32), rng.uniform(-1, 1, self.n).astype(np.float32)]
+
+    def work(self):
+        return 8.0 * self.n + 4
+
+    def cpu_sample(self, host):
+        import oracle
+
+        a, b = host
+        t = _best_of(lambda: oracle.ref_dot(a, b), 3)
+        return {"value": self.work() / t / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
+                "sample": "full 2^24 dot, the reference's emitted C (sequential left fold, 1 thread), best of 3"}
+
+
+class Conv(Workload):
+    key = "conv"
+    program = "padClamp2D + slide2D + map/reduce 3x3 (programs.CONV)"
+    config_index = 3
+    n = m = 8192
+    metric_unit = "GB/s"
+    bound = "hbm"
+
+    def compile(self):
+        from paper_2201_03611_b200 import programs
+
+        return programs.compile_config(self.key), {"n": self.n, "m": self.m}
+
+    def inputs(self):
+        rng = np.random.default_rng(self.config_index + 1000 * self.rank)
+        img = rng.uniform(-1, 1, (self.n, self.m)).astype(np.float32)
+        w = (np.array([[1, 2, 1], [2, 4, 2], [1, 2, 1]], np.float32) / 16).astype(np.float32)
+        return [img, w]
+
+    def work(self):
+        return 4.0 * (2 * self.n * self.m + 9)
+
+    def cpu_sample(self, host):
+        import oracle
+
+        img, w = host
+        rows = 1024
+        t = _best_of(lambda: oracle.conv3x3(img[:rows], w), 3)
+        return {"value": 4.0 * 2 * rows * self.m / t / 1e9, "unit": "GB/s", "cores": oracle.threads(),
+                "kind": "port", "sample": f"{rows}x{self.m} band, C restatement (oracle/rise_oracle.c), OpenMP"}
+
+
+class Sgemm(Workload):
+    key = "sgemm"
+    program = "A |> mapGlobal(arow => Bt |> mapGlobal(brow => zip |> reduceSeq)) (programs.SGEMM_BT)"
+    config_index = 4
+    n = m = k = 4096
+    metric_unit = "GFLOP/s"
+    bound = "tensor"
+
+    def compile(self):
+        from paper_2201_03611_b200 import programs
+
+        return programs.compile_config(self.key), {"n": self.n, "m": self.m, "k": self.k}
+
+    def inputs(self):
+        rng = np.random.default_rng(self.config_index + 1000 * self.rank)
+        A = rng.uniform(-1, 1, (self.n, self.k)).astype(np.float32)
+        Bt = rng.uniform(-1, 1, (self.m, self.k)).astype(np.float32)
+        return [A, Bt]
+
+    def work(self):
+        return 2.0 * self.n * self.m * self.k
+
+    def cpu_sample(self, host):
+        import oracle
+
+        A, Bt = host
+        rows = 64
+        t = _best_of(lambda: oracle.ref_sgemm_bt(A[:rows], Bt), 2)
+        return {"value": 2.0 * rows * self.m * self.k / t / 1e9, "unit": "GFLOP/s", "cores": oracle.threads(),
+                "kind": "reference",
+                "sample": f"{rows} rows of the 4096^3 sgemm, the reference's emitted OpenMP C (oracle/_ref)"}
+
+
+class Nbody(Workload):
+    key = "nbody"
+    program = "all-pairs map/reduce + Euler velocity step (programs.NBODY)"
+    config_index = 5
+    n = 131072
+    metric_unit = "GFLOP/s"
+    bound = "fp32-simt"
+
+    def compile(self):
+        from paper_2201_03611_b200 import programs
+
+        return programs.compile_config(self.key), {"n": self.n}
+
+    def inputs(self):
+        rng = np.random.default_rng(self.config_index + 1000 * self.rank)
+        pos = rng.uniform(-1, 1, (self.n, 3)).astype(np.float32)
+        vel = np.zeros((self.n, 3), np.float32)
+        mass = rng.uniform(0.5, 1.5, self.n).astype(np.float32)
+        return [pos, vel, mass]
+
+    def work(self):
+        return 20.0 * self.n * self.n
+
+    def cpu_sample(self, host):
+        import oracle
+
+        pos, vel, mass = host
+        count = 256
+        t = _best_of(lambda: oracle.nbody(pos, vel, mass, 0, count), 2)
+        return {"value": 20.0 * count * self.n / t / 1e9, "unit": "GFLOP/s", "cores": oracle.threads(),
+                "kind": "port", "sample": f"{count} target bodies x {self.n} sources, C restatement, OpenMP"}
+
+
+WORKLOADS = {w.key: w for w in (Gemv, GemvOpt, Dot, Conv, Sgemm, Nbody)}
+
+
+def _best_of(fn, k):
+    best = math.inf
+    for _ in range(k):
+        t0 = time.perf_counter()
+        fn()
+        best = min(best, time.perf_counter() - t0)
+    return best
+
+
+# ---------------------------------------------------------------------------
+# clocks (sampled during the timed region)
+
+
+class ClockSampler:
+    def __init__(self, device_index: int, period_s=0.002):
+        self.samples = []
+        self.reasons = set()
+        self.period = period_s
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception:  # noqa: BLE001
+            self.max_mhz = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    _REASONS = {
+        0x0000000000000002: "applications_clocks_setting",
+        0x0000000000000004: "sw_power_cap",
+        0x0000000000000008: "hw_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000080: "hw_power_brake_slowdown",
+    }
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self._REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._ok:
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._ok:
+            self._t.join(timeout=1)
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2201_03611_b200 import emit_cuda
+    from paper_2201_03611_b200.run import Executable
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    wl = WORKLOADS[args.workload](rank, world)
+    compiled, nats = wl.compile()
+    code = emit_cuda(compiled.unit)
+    exe = Executable(code, nats, device=local_rank)
+    host = wl.inputs()
+    stream = torch.cuda.Stream()
+    dev_in = [torch.from_numpy(h.reshape(-1)).to("cuda") for h in host]
+    out = torch.empty(exe.output_size, dtype=torch.float32, device="cuda")
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    n_stages = len(exe.kernels)
+
+    def step():
+        exe(*dev_in, out=out, stream=stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            flush.zero_()
+            step()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clocks:
+        for s in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                starts[s].record(stream)
+                step()
+                ends[s].record(stream)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+    per_step = [starts[s].elapsed_time(ends[s]) for s in range(args.steps)]
+    total_ms = float(sum(per_step))
+    if dist is not None:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+    value = wl.work() * world / (ms * 1e-3) / 1e9
+
+    # e2e: pinned host -> device, launch, device -> host, every step
+    pinned = [torch.from_numpy(h.reshape(-1)).pin_memory() for h in host]
+    host_out = torch.empty(exe.output_size, dtype=torch.float32).pin_memory()
+    e2e_steps = max(3, min(args.steps, 10))
+    for _ in range(2):
+        exe.run_host(pinned, host_out, dev_in, out, stream)
+    stream.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        exe.run_host(pinned, host_out, dev_in, out, stream)
+    e1.record(stream)
+    stream.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d = int(sum(h.nbytes for h in host))
+    d2h = int(exe.output_size * 4)
+
+    result = None
+    if rank == 0:
+        peaks = _peaks()
+        achieved = wl.work() / (ms * 1e-3) / 1e9  # per GPU, per launch-set
+        roof = _roofline(wl, achieved, peaks, args)
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = wl.cpu_sample(host)
+        result = {
+            "metric": f"{wl.key} {wl.metric_unit} (per-benchmark GFLOP/s or GB/s vs B200 roofline)",
+            "value": round(value, 3),
+            "unit": wl.metric_unit,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms, 6),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (numpy default_rng seeded by config index; uniform(-1,1))",
+            "config": {
+                "workload": f"{wl.key}: BASELINE.json configs[{wl.config_index - 1}]",
+                "program": wl.program,
+                "sizes": nats,
+                "kernels": exe.kernel_names,
+                "templates": exe.template_kinds,
+                "l2": "flushed between steps (256 MiB write, outside the events)",
+                "parallelism": f"weak scaling: each of {world} rank(s) runs its own full-size instance"
+                               if world > 1 else "1 GPU",
+            },
+            "e2e": {"value": round(wl.work() * world / (e2e_ms * 1e-3) / 1e9, 3), "unit": wl.metric_unit,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": round(e2e_ms, 4),
+                    "path": "Executable.run_host: pinned H2D + launch + D2H on one stream"},
+            "gpu_launches": args.steps * n_stages,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+        }
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result
+
+
+def _roofline(wl, achieved, peaks, args):
+    if wl.bound == "hbm":
+        peak, unit, src = peaks["hbm_gbs"], "GB/s", peaks["source"]
+    elif wl.bound == "tensor":
+        peak, unit, src = _tf32_peak() / 3.0, "GFLOP/s", "measured cuBLAS TF32 / 3 (3xTF32 fp32-equivalent)"
+    else:
+        peak, unit, src = FP32_SIMT_TFLOPS * 1e3, "GFLOP/s", "derived 148 SM x 128 x 2 x 1.965 GHz"
+    traffic = None
+    summary = ROOT / "profiles" / f"ncu_{wl.key}.json"
+    if summary.exists():
+        try:
+            traffic = json.loads(summary.read_text()).get("dram_bytes_per_launch")
+        except Exception:  # noqa: BLE001
+            traffic = None
+    return {"bound": wl.bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
+            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": src,
+            "algorithmic_work_per_launch": wl.work()}
+
+
+def _tf32_peak():
+    import torch
+
+    torch.backends.cuda.matmul.allow_tf32 = True
+    a = torch.randn(8192, 8192, device="cuda")
+    b = torch.randn(8192, 8192, device="cuda")
+    for _ in range(3):
+        a @ b
+    torch.cuda.synchronize()
+    best = math.inf
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return 2 * 8192 ** 3 / (best * 1e-3) / 1e9
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's own CPU implementation
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    import oracle
+
+    wl = WORKLOADS[args.workload](0, 1)
+    host = wl.inputs()
+    if oracle.ref_lib() is None and wl.key in ("gemv", "gemv_opt", "dot", "sgemm"):
+        return {"impl": "reference", "unavailable": "oracle/_ref (the reference's emitted C) was not built"}
+    for _ in range(args.warmup):
+        wl.cpu_sample(host)
+    t0 = time.perf_counter()
+    vals = []
+    sample = None
+    for _ in range(args.steps):
+        sample = wl.cpu_sample(host)
+        vals.append(sample["value"])
+    elapsed = time.perf_counter() - t0
+    value = float(np.median(vals))
+    return {
+        "impl": "reference",
+        "metric": f"{wl.key} {wl.metric_unit} (per-benchmark GFLOP/s or GB/s vs B200 roofline)",
+        "value": round(value, 3),
+        "unit": sample["unit"],
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(1e3 * elapsed / args.steps, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (numpy default_rng seeded by config index; uniform(-1,1))",
+        "config": {"workload": f"{wl.key}: BASELINE.json configs[{wl.config_index - 1}]", "program": wl.program},
+        "cpu_baseline": {"value": round(value, 3), "unit": sample["unit"], "cores": sample["cores"],
+                         "kind": sample["kind"], "sample": sample["sample"]},
+        "e2e": {"value": round(value, 3), "unit": sample["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="gemv")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(1)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+    else:
+        res = run_ours(args, rank, world, local_rank)
+    if rank == 0 and res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,143 @@
+/*
+ * rise_b200.h — C ABI of the B200 (sm_100a) execution backend for RISE/Shine.
+ *
+ * This is the drop-in boundary that replaces the reference's execution stage
+ * for emitted kernels.  In the reference (pure Python, package `risec`):
+ *
+ *   codegen.emit(unit, target)                -> kernel text      (codegen.py:451)
+ *   cexec.execute_kernel(source, arguments)   -> runs the text    (cexec.py:509)
+ *   cexec.run_emitted(code, unit, nats, ins)  -> nested result    (cexec.py:555)
+ *
+ * Here the kernel text is CUDA C++ for sm_100a, compiled at run time with
+ * NVRTC, and executed through the entry points below.  The Python side
+ * (`paper_2201_03611_b200.runtime`) binds them with ctypes; INTEGRATION.md
+ * shows the binding a maintainer of the reference would add.
+ *
+ * Conventions (mirroring the reference's error model, errors.py:10-80):
+ *   - every function returns int status: 0 = ok, nonzero = failure;
+ *   - the failure text is available from rs_last_error() (thread-local);
+ *   - the Python wrapper raises EmitError (stage "emit") for compile
+ *     failures and InterpreterError (stage "run") for launch / memory
+ *     failures, exactly the classes the reference raises from emit()
+ *     (codegen.py:453-454) and execute_kernel() (cexec.py:516, 376, 495).
+ *   - plain pointers and sizes only; no torch types cross this boundary.
+ *   - device pointers are CUdeviceptr values carried as void*; streams and
+ *     events are CUstream / CUevent handles carried as void*.  The runtime
+ *     runs in the device's primary context, so buffers allocated by any
+ *     other user of the primary context (e.g. PyTorch) are valid arguments.
+ */
+#ifndef RISE_B200_H
+#define RISE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rs_module_s* rs_module;
+typedef struct rs_function_s* rs_function;
+
+/* ---- status / device ------------------------------------------------- */
+
+/* Thread-local text of the last failure (never NULL). */
+const char* rs_last_error(void);
+
+/* ABI version of this library (bumped on any signature change). */
+int rs_abi_version(void);
+
+/* Load the CUDA driver (dlopen libcuda.so.1), init it and make `device`'s
+ * primary context current on the calling thread.  Idempotent.
+ * Replaces: nothing in the reference — cexec has no device (cexec.py:36-43
+ * sequentialises the device id intrinsics instead). */
+int rs_init(int device);
+
+int rs_device_count(int* count);
+
+/* CUdevice_attribute query on the current device (e.g. 16 = SM count). */
+int rs_device_attribute(int attribute, int* value);
+
+/* NVRTC version, for the build report. */
+int rs_nvrtc_version(int* major, int* minor);
+
+/* ---- compilation (replaces cexec.parse_kernel, cexec.py:97) ---------- */
+
+/* Compile CUDA C++ `source` with NVRTC for sm_100a into a CUBIN and load it.
+ * `opts` are NVRTC options (the architecture option is added if absent).
+ * `name_exprs` are the kernel name expressions to instantiate (template
+ * kernels such as "mvKernel<8192, 8192>"); their lowered (mangled) names are
+ * available through rs_module_lowered_name in the same order.
+ * Compile failure: status != 0 and the NVRTC log in rs_last_error(). */
+int rs_compile(const char* source, const char* program_name,
+               const char* const* opts, int nopts,
+               const char* const* name_exprs, int nexprs,
+               rs_module* out_module);
+
+/* Compile only (no device needed): returns the CUBIN image in a buffer owned
+ * by the caller-visible handle; used by build() and the CPU test-suite. */
+int rs_compile_cubin(const char* source, const char* program_name,
+                     const char* const* opts, int nopts,
+                     const char* const* name_exprs, int nexprs,
+                     void** out_image, size_t* out_size,
+                     char** out_lowered_names /* '\n'-separated, malloc'd */,
+                     char** out_log /* malloc'd */);
+void rs_free_host(void* p);
+
+/* Load a previously compiled CUBIN image (on-disk cache). */
+int rs_module_load(const void* image, size_t size, rs_module* out_module);
+
+int rs_module_lowered_name(rs_module m, int index, const char** out_name);
+int rs_module_get_function(rs_module m, const char* lowered_name, rs_function* out_fn);
+int rs_module_unload(rs_module m);
+
+/* CUfunction_attribute query (e.g. 4 = NUM_REGS, 1 = SHARED_SIZE_BYTES). */
+int rs_function_attribute(rs_function f, int attribute, int* value);
+
+/* ---- launch (replaces cexec.execute_kernel's _exec_block, cexec.py:526) */
+
+/* Launch `f` with grid/block dims, an optional thread-block-cluster shape
+ * (cluster == NULL or {1,1,1} for none), `smem` bytes of dynamic shared
+ * memory (the >48 KB opt-in attribute is set automatically) on `stream`
+ * (NULL = legacy default stream).  `args` follows cuLaunchKernel's
+ * kernelParams convention: an array of pointers to each argument value. */
+int rs_launch(rs_function f, const unsigned grid[3], const unsigned block[3],
+              const unsigned cluster[3], unsigned smem, void* stream, void** args);
+
+/* ---- memory (replaces cexec.flatten_value/unflatten_value, cexec.py:533-552) */
+
+int rs_malloc(void** dptr, size_t bytes);
+int rs_free(void* dptr);
+int rs_memcpy_htod(void* dst, const void* src, size_t bytes, void* stream);
+int rs_memcpy_dtoh(void* dst, const void* src, size_t bytes, void* stream);
+int rs_memcpy_dtod(void* dst, const void* src, size_t bytes, void* stream);
+int rs_memset_d8(void* dst, unsigned char value, size_t bytes, void* stream);
+
+/* ---- streams / events ------------------------------------------------ */
+
+int rs_stream_create(void** stream);
+int rs_stream_destroy(void* stream);
+int rs_stream_synchronize(void* stream);
+int rs_device_synchronize(void);
+int rs_event_create(void** event);
+int rs_event_destroy(void* event);
+int rs_event_record(void* event, void* stream);
+int rs_event_synchronize(void* event);
+int rs_event_elapsed_ms(float* ms, void* start, void* end);
+
+/* ---- TMA ------------------------------------------------------------- */
+
+/* Encode a 2-D (inner dim0, outer dim1) tiled TMA descriptor for fp32 data
+ * into the 128-byte buffer `desc` (CUtensorMap layout).  `row_stride_bytes`
+ * is the byte distance between consecutive dim1 rows (multiple of 16).
+ * `swizzle`: 0 none, 1 32B, 2 64B, 3 128B.  Out-of-bounds box elements are
+ * zero-filled by the hardware. */
+int rs_tma_desc_2d_f32(void* desc, const void* base,
+                       uint64_t dim0, uint64_t dim1, uint64_t row_stride_bytes,
+                       uint32_t box0, uint32_t box1, int swizzle);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RISE_B200_H */

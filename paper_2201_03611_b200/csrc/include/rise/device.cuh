@@ -1,0 +1,90 @@
+// rise/device.cuh — device helpers shared by every emitted sm_100a kernel.
+// NVRTC-compiled (no host headers); included by the text emit_cuda produces.
+#pragma once
+
+#define RS_DEVICE __device__ __forceinline__
+
+// padClamp index: min(max(k, 0), hi)  (extension.py semantics of padClamp)
+RS_DEVICE int rs_clamp(int k, int hi) { return k < 0 ? 0 : (k > hi ? hi : k); }
+
+// integer power for Pow sizes (the reference's ipow helper, codegen.py:38-44)
+RS_DEVICE int rs_ipow(int base, int e) {
+  int r = 1;
+  while (e > 0) { r *= base; --e; }
+  return r;
+}
+
+// IEEE binary32 reciprocal square root with both steps correctly rounded:
+// bit-exact with the oracle definition rsqrt(x) = 1.0f / sqrt(x).
+RS_DEVICE float rs_rsqrt_exact(float x) { return __fdiv_rn(1.0f, __fsqrt_rn(x)); }
+
+// Fast path (MUFU.RSQ); used only where the program is compared under a
+// tolerance (DESIGN.md parity rules).
+RS_DEVICE float rs_rsqrt_fast(float x) { return rsqrtf(x); }
+
+RS_DEVICE unsigned rs_smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// ---- mbarrier / bulk-copy (TMA) primitives ---------------------------------
+
+RS_DEVICE void rs_mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(rs_smem_addr(bar)), "r"(count) : "memory");
+}
+
+RS_DEVICE void rs_fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+RS_DEVICE void rs_fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+RS_DEVICE void rs_mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(rs_smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+RS_DEVICE void rs_mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(rs_smem_addr(bar)) : "memory");
+}
+
+RS_DEVICE bool rs_mbar_try_wait(unsigned long long* bar, unsigned phase) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(rs_smem_addr(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+
+RS_DEVICE void rs_mbar_wait(unsigned long long* bar, unsigned phase) {
+  while (!rs_mbar_try_wait(bar, phase)) {
+  }
+}
+
+// 1-D bulk copy global -> shared (TMA engine), completion counted in bytes on
+// `bar`.  src, dst and bytes must be multiples of 16.
+RS_DEVICE void rs_bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          rs_smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(rs_smem_addr(bar))
+      : "memory");
+}
+
+// 128-bit streaming global load that does not allocate in L1.
+RS_DEVICE float4 rs_ldg_stream(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+RS_DEVICE unsigned rs_lane() { return threadIdx.x & 31u; }
+RS_DEVICE unsigned rs_warp() { return threadIdx.x >> 5; }

@@ -1,0 +1,488 @@
+// rise_runtime.cpp — native runtime behind include/rise_b200.h.
+//
+// NVRTC compiles kernel text to sm_100a CUBIN; the CUDA driver API (loaded
+// with dlopen so the library also loads on GPU-less build hosts) loads the
+// module and launches it with cuLaunchKernelEx (thread-block clusters, large
+// dynamic shared memory).  Runs in the primary context so device buffers are
+// interchangeable with any other primary-context user.
+//
+// Reference counterpart: cexec.py (the Python evaluator of emitted C text),
+// cexec.py:97 parse_kernel -> rs_compile, cexec.py:509 execute_kernel ->
+// rs_launch, cexec.py:533-552 flatten/unflatten -> rs_memcpy_*.
+
+#include "../../include/rise_b200.h"
+
+#include <cuda.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err = "";
+
+int fail(const char* fmt, ...) {
+  char buf[4096];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return 1;
+}
+
+// ---- driver API table (dlopen'd) ----------------------------------------
+struct Driver {
+  bool loaded = false;
+  void* handle = nullptr;
+  CUresult (*Init)(unsigned);
+  CUresult (*DeviceGet)(CUdevice*, int);
+  CUresult (*DeviceGetCount)(int*);
+  CUresult (*DeviceGetAttribute)(int*, CUdevice_attribute, CUdevice);
+  CUresult (*DevicePrimaryCtxRetain)(CUcontext*, CUdevice);
+  CUresult (*CtxSetCurrent)(CUcontext);
+  CUresult (*CtxSynchronize)(void);
+  CUresult (*ModuleLoadData)(CUmodule*, const void*);
+  CUresult (*ModuleUnload)(CUmodule);
+  CUresult (*ModuleGetFunction)(CUfunction*, CUmodule, const char*);
+  CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int);
+  CUresult (*FuncGetAttribute)(int*, CUfunction_attribute, CUfunction);
+  CUresult (*LaunchKernelEx)(const CUlaunchConfig*, CUfunction, void**, void**);
+  CUresult (*MemAlloc)(CUdeviceptr*, size_t);
+  CUresult (*MemFree)(CUdeviceptr);
+  CUresult (*MemcpyHtoDAsync)(CUdeviceptr, const void*, size_t, CUstream);
+  CUresult (*MemcpyDtoHAsync)(void*, CUdeviceptr, size_t, CUstream);
+  CUresult (*MemcpyDtoDAsync)(CUdeviceptr, CUdeviceptr, size_t, CUstream);
+  CUresult (*MemsetD8Async)(CUdeviceptr, unsigned char, size_t, CUstream);
+  CUresult (*StreamCreate)(CUstream*, unsigned);
+  CUresult (*StreamDestroy)(CUstream);
+  CUresult (*StreamSynchronize)(CUstream);
+  CUresult (*EventCreate)(CUevent*, unsigned);
+  CUresult (*EventDestroy)(CUevent);
+  CUresult (*EventRecord)(CUevent, CUstream);
+  CUresult (*EventSynchronize)(CUevent);
+  CUresult (*EventElapsedTime)(float*, CUevent, CUevent);
+  CUresult (*TensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  CUresult (*GetErrorString)(CUresult, const char**);
+};
+
+Driver g_drv;
+std::mutex g_mu;
+CUcontext g_ctx = nullptr;
+CUdevice g_dev = 0;
+bool g_inited = false;
+
+template <typename F>
+bool sym(F& fn, const char* name) {
+  fn = reinterpret_cast<F>(dlsym(g_drv.handle, name));
+  return fn != nullptr;
+}
+
+int load_driver() {
+  if (g_drv.loaded) return 0;
+  g_drv.handle = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+  if (!g_drv.handle) g_drv.handle = dlopen("libcuda.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!g_drv.handle) return fail("rs_init: cannot load the CUDA driver (libcuda.so.1): %s", dlerror());
+  bool ok = true;
+  ok &= sym(g_drv.Init, "cuInit");
+  ok &= sym(g_drv.DeviceGet, "cuDeviceGet");
+  ok &= sym(g_drv.DeviceGetCount, "cuDeviceGetCount");
+  ok &= sym(g_drv.DeviceGetAttribute, "cuDeviceGetAttribute");
+  ok &= sym(g_drv.DevicePrimaryCtxRetain, "cuDevicePrimaryCtxRetain");
+  ok &= sym(g_drv.CtxSetCurrent, "cuCtxSetCurrent");
+  ok &= sym(g_drv.CtxSynchronize, "cuCtxSynchronize");
+  ok &= sym(g_drv.ModuleLoadData, "cuModuleLoadData");
+  ok &= sym(g_drv.ModuleUnload, "cuModuleUnload");
+  ok &= sym(g_drv.ModuleGetFunction, "cuModuleGetFunction");
+  ok &= sym(g_drv.FuncSetAttribute, "cuFuncSetAttribute");
+  ok &= sym(g_drv.FuncGetAttribute, "cuFuncGetAttribute");
+  ok &= sym(g_drv.LaunchKernelEx, "cuLaunchKernelEx");
+  ok &= sym(g_drv.MemAlloc, "cuMemAlloc_v2");
+  ok &= sym(g_drv.MemFree, "cuMemFree_v2");
+  ok &= sym(g_drv.MemcpyHtoDAsync, "cuMemcpyHtoDAsync_v2");
+  ok &= sym(g_drv.MemcpyDtoHAsync, "cuMemcpyDtoHAsync_v2");
+  ok &= sym(g_drv.MemcpyDtoDAsync, "cuMemcpyDtoDAsync_v2");
+  ok &= sym(g_drv.MemsetD8Async, "cuMemsetD8Async");
+  ok &= sym(g_drv.StreamCreate, "cuStreamCreate");
+  ok &= sym(g_drv.StreamDestroy, "cuStreamDestroy_v2");
+  ok &= sym(g_drv.StreamSynchronize, "cuStreamSynchronize");
+  ok &= sym(g_drv.EventCreate, "cuEventCreate");
+  ok &= sym(g_drv.EventDestroy, "cuEventDestroy_v2");
+  ok &= sym(g_drv.EventRecord, "cuEventRecord");
+  ok &= sym(g_drv.EventSynchronize, "cuEventSynchronize");
+  ok &= sym(g_drv.EventElapsedTime, "cuEventElapsedTime");
+  ok &= sym(g_drv.TensorMapEncodeTiled, "cuTensorMapEncodeTiled");
+  ok &= sym(g_drv.GetErrorString, "cuGetErrorString");
+  if (!ok) return fail("rs_init: the CUDA driver lacks a required entry point");
+  g_drv.loaded = true;
+  return 0;
+}
+
+int cu_check(CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return 0;
+  const char* s = "unknown";
+  if (g_drv.GetErrorString) g_drv.GetErrorString(r, &s);
+  return fail("%s failed: %s (CUresult %d)", what, s, (int)r);
+}
+
+#define CU(call, what)                         \
+  do {                                         \
+    if (int _e = cu_check((call), (what))) return _e; \
+  } while (0)
+
+int ensure_ctx() {
+  if (!g_inited) return fail("rs_init has not been called");
+  return cu_check(g_drv.CtxSetCurrent(g_ctx), "cuCtxSetCurrent");
+}
+
+}  // namespace
+
+struct rs_module_s {
+  CUmodule mod = nullptr;
+  std::vector<std::string> lowered;
+};
+
+struct rs_function_s {
+  CUfunction fn = nullptr;
+  int smem_optin = 0;  // dynamic smem bytes already enabled via attribute
+};
+
+extern "C" {
+
+const char* rs_last_error(void) { return g_err.c_str(); }
+
+int rs_abi_version(void) { return 1; }
+
+int rs_init(int device) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  if (int e = load_driver()) return e;
+  if (g_inited) {
+    if (device != (int)g_dev) return fail("rs_init: already initialised on device %d", (int)g_dev);
+    return cu_check(g_drv.CtxSetCurrent(g_ctx), "cuCtxSetCurrent");
+  }
+  CU(g_drv.Init(0), "cuInit");
+  int count = 0;
+  CU(g_drv.DeviceGetCount(&count), "cuDeviceGetCount");
+  if (device < 0 || device >= count) return fail("rs_init: device %d out of range (%d devices)", device, count);
+  CU(g_drv.DeviceGet(&g_dev, device), "cuDeviceGet");
+  CU(g_drv.DevicePrimaryCtxRetain(&g_ctx, g_dev), "cuDevicePrimaryCtxRetain");
+  CU(g_drv.CtxSetCurrent(g_ctx), "cuCtxSetCurrent");
+  g_inited = true;
+  return 0;
+}
+
+int rs_device_count(int* count) {
+  if (int e = load_driver()) return e;
+  CU(g_drv.Init(0), "cuInit");
+  CU(g_drv.DeviceGetCount(count), "cuDeviceGetCount");
+  return 0;
+}
+
+int rs_device_attribute(int attribute, int* value) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.DeviceGetAttribute(value, (CUdevice_attribute)attribute, g_dev), "cuDeviceGetAttribute");
+  return 0;
+}
+
+int rs_nvrtc_version(int* major, int* minor) {
+  if (nvrtcVersion(major, minor) != NVRTC_SUCCESS) return fail("nvrtcVersion failed");
+  return 0;
+}
+
+void rs_free_host(void* p) { free(p); }
+
+int rs_compile_cubin(const char* source, const char* program_name, const char* const* opts, int nopts,
+                     const char* const* name_exprs, int nexprs, void** out_image, size_t* out_size,
+                     char** out_lowered_names, char** out_log) {
+  *out_image = nullptr;
+  *out_size = 0;
+  if (out_lowered_names) *out_lowered_names = nullptr;
+  if (out_log) *out_log = nullptr;
+  nvrtcProgram prog;
+  nvrtcResult r = nvrtcCreateProgram(&prog, source, program_name ? program_name : "rise.cu", 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) return fail("nvrtcCreateProgram: %s", nvrtcGetErrorString(r));
+  for (int i = 0; i < nexprs; ++i) {
+    r = nvrtcAddNameExpression(prog, name_exprs[i]);
+    if (r != NVRTC_SUCCESS) {
+      nvrtcDestroyProgram(&prog);
+      return fail("nvrtcAddNameExpression(%s): %s", name_exprs[i], nvrtcGetErrorString(r));
+    }
+  }
+  std::vector<const char*> all;
+  bool has_arch = false;
+  for (int i = 0; i < nopts; ++i) {
+    all.push_back(opts[i]);
+    if (strstr(opts[i], "arch") != nullptr) has_arch = true;
+  }
+  if (!has_arch) all.push_back("--gpu-architecture=sm_100a");
+  nvrtcResult cr = nvrtcCompileProgram(prog, (int)all.size(), all.data());
+  size_t log_size = 0;
+  nvrtcGetProgramLogSize(prog, &log_size);
+  std::string log(log_size, '\0');
+  if (log_size) nvrtcGetProgramLog(prog, &log[0]);
+  if (out_log) {
+    *out_log = (char*)malloc(log.size() + 1);
+    memcpy(*out_log, log.c_str(), log.size() + 1);
+  }
+  if (cr != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return fail("NVRTC compilation of %s failed (%s):\n%s", program_name ? program_name : "rise.cu",
+                nvrtcGetErrorString(cr), log.c_str());
+  }
+  std::string names;
+  for (int i = 0; i < nexprs; ++i) {
+    const char* lowered = nullptr;
+    r = nvrtcGetLoweredName(prog, name_exprs[i], &lowered);
+    if (r != NVRTC_SUCCESS || !lowered) {
+      nvrtcDestroyProgram(&prog);
+      return fail("nvrtcGetLoweredName(%s): %s", name_exprs[i], nvrtcGetErrorString(r));
+    }
+    names += lowered;
+    names += '\n';
+  }
+  size_t size = 0;
+  r = nvrtcGetCUBINSize(prog, &size);
+  if (r != NVRTC_SUCCESS || size == 0) {
+    nvrtcDestroyProgram(&prog);
+    return fail("nvrtcGetCUBINSize: %s (compile with a real sm_ architecture)", nvrtcGetErrorString(r));
+  }
+  void* image = malloc(size);
+  r = nvrtcGetCUBIN(prog, (char*)image);
+  nvrtcDestroyProgram(&prog);
+  if (r != NVRTC_SUCCESS) {
+    free(image);
+    return fail("nvrtcGetCUBIN: %s", nvrtcGetErrorString(r));
+  }
+  *out_image = image;
+  *out_size = size;
+  if (out_lowered_names) {
+    *out_lowered_names = (char*)malloc(names.size() + 1);
+    memcpy(*out_lowered_names, names.c_str(), names.size() + 1);
+  }
+  return 0;
+}
+
+int rs_module_load(const void* image, size_t size, rs_module* out_module) {
+  (void)size;
+  if (int e = ensure_ctx()) return e;
+  CUmodule mod;
+  CU(g_drv.ModuleLoadData(&mod, image), "cuModuleLoadData");
+  auto* m = new rs_module_s();
+  m->mod = mod;
+  *out_module = m;
+  return 0;
+}
+
+int rs_compile(const char* source, const char* program_name, const char* const* opts, int nopts,
+               const char* const* name_exprs, int nexprs, rs_module* out_module) {
+  void* image = nullptr;
+  size_t size = 0;
+  char* names = nullptr;
+  if (int e = rs_compile_cubin(source, program_name, opts, nopts, name_exprs, nexprs, &image, &size, &names,
+                               nullptr))
+    return e;
+  rs_module m = nullptr;
+  int e = rs_module_load(image, size, &m);
+  free(image);
+  if (e) {
+    free(names);
+    return e;
+  }
+  std::string all(names ? names : "");
+  free(names);
+  size_t pos = 0;
+  while (pos < all.size()) {
+    size_t nl = all.find('\n', pos);
+    if (nl == std::string::npos) nl = all.size();
+    m->lowered.push_back(all.substr(pos, nl - pos));
+    pos = nl + 1;
+  }
+  *out_module = m;
+  return 0;
+}
+
+int rs_module_lowered_name(rs_module m, int index, const char** out_name) {
+  if (!m || index < 0 || index >= (int)m->lowered.size()) return fail("rs_module_lowered_name: bad index %d", index);
+  *out_name = m->lowered[index].c_str();
+  return 0;
+}
+
+int rs_module_get_function(rs_module m, const char* lowered_name, rs_function* out_fn) {
+  if (int e = ensure_ctx()) return e;
+  CUfunction fn;
+  CU(g_drv.ModuleGetFunction(&fn, m->mod, lowered_name), "cuModuleGetFunction");
+  auto* f = new rs_function_s();
+  f->fn = fn;
+  *out_fn = f;
+  return 0;
+}
+
+int rs_module_unload(rs_module m) {
+  if (!m) return 0;
+  if (g_inited && m->mod) g_drv.ModuleUnload(m->mod);
+  delete m;
+  return 0;
+}
+
+int rs_function_attribute(rs_function f, int attribute, int* value) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.FuncGetAttribute(value, (CUfunction_attribute)attribute, f->fn), "cuFuncGetAttribute");
+  return 0;
+}
+
+int rs_launch(rs_function f, const unsigned grid[3], const unsigned block[3], const unsigned cluster[3],
+              unsigned smem, void* stream, void** args) {
+  if (int e = ensure_ctx()) return e;
+  if (smem > 48 * 1024 && (int)smem > f->smem_optin) {
+    CU(g_drv.FuncSetAttribute(f->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem),
+       "cuFuncSetAttribute(MAX_DYNAMIC_SHARED_SIZE_BYTES)");
+    f->smem_optin = (int)smem;
+  }
+  CUlaunchConfig cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDimX = grid[0];
+  cfg.gridDimY = grid[1];
+  cfg.gridDimZ = grid[2];
+  cfg.blockDimX = block[0];
+  cfg.blockDimY = block[1];
+  cfg.blockDimZ = block[2];
+  cfg.sharedMemBytes = smem;
+  cfg.hStream = (CUstream)stream;
+  CUlaunchAttribute attr[1];
+  if (cluster && (cluster[0] * cluster[1] * cluster[2]) > 1) {
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+    attr[0].value.clusterDim.x = cluster[0];
+    attr[0].value.clusterDim.y = cluster[1];
+    attr[0].value.clusterDim.z = cluster[2];
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  CU(g_drv.LaunchKernelEx(&cfg, f->fn, args, nullptr), "cuLaunchKernelEx");
+  return 0;
+}
+
+int rs_malloc(void** dptr, size_t bytes) {
+  if (int e = ensure_ctx()) return e;
+  CUdeviceptr p = 0;
+  CU(g_drv.MemAlloc(&p, bytes ? bytes : 1), "cuMemAlloc");
+  *dptr = (void*)p;
+  return 0;
+}
+
+int rs_free(void* dptr) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.MemFree((CUdeviceptr)dptr), "cuMemFree");
+  return 0;
+}
+
+int rs_memcpy_htod(void* dst, const void* src, size_t bytes, void* stream) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.MemcpyHtoDAsync((CUdeviceptr)dst, src, bytes, (CUstream)stream), "cuMemcpyHtoDAsync");
+  return 0;
+}
+
+int rs_memcpy_dtoh(void* dst, const void* src, size_t bytes, void* stream) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.MemcpyDtoHAsync(dst, (CUdeviceptr)src, bytes, (CUstream)stream), "cuMemcpyDtoHAsync");
+  return 0;
+}
+
+int rs_memcpy_dtod(void* dst, const void* src, size_t bytes, void* stream) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.MemcpyDtoDAsync((CUdeviceptr)dst, (CUdeviceptr)src, bytes, (CUstream)stream), "cuMemcpyDtoDAsync");
+  return 0;
+}
+
+int rs_memset_d8(void* dst, unsigned char value, size_t bytes, void* stream) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.MemsetD8Async((CUdeviceptr)dst, value, bytes, (CUstream)stream), "cuMemsetD8Async");
+  return 0;
+}
+
+int rs_stream_create(void** stream) {
+  if (int e = ensure_ctx()) return e;
+  CUstream s;
+  CU(g_drv.StreamCreate(&s, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+  *stream = (void*)s;
+  return 0;
+}
+
+int rs_stream_destroy(void* stream) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.StreamDestroy((CUstream)stream), "cuStreamDestroy");
+  return 0;
+}
+
+int rs_stream_synchronize(void* stream) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.StreamSynchronize((CUstream)stream), "cuStreamSynchronize");
+  return 0;
+}
+
+int rs_device_synchronize(void) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.CtxSynchronize(), "cuCtxSynchronize");
+  return 0;
+}
+
+int rs_event_create(void** event) {
+  if (int e = ensure_ctx()) return e;
+  CUevent ev;
+  CU(g_drv.EventCreate(&ev, CU_EVENT_DEFAULT), "cuEventCreate");
+  *event = (void*)ev;
+  return 0;
+}
+
+int rs_event_destroy(void* event) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.EventDestroy((CUevent)event), "cuEventDestroy");
+  return 0;
+}
+
+int rs_event_record(void* event, void* stream) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.EventRecord((CUevent)event, (CUstream)stream), "cuEventRecord");
+  return 0;
+}
+
+int rs_event_synchronize(void* event) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.EventSynchronize((CUevent)event), "cuEventSynchronize");
+  return 0;
+}
+
+int rs_event_elapsed_ms(float* ms, void* start, void* end) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.EventElapsedTime(ms, (CUevent)start, (CUevent)end), "cuEventElapsedTime");
+  return 0;
+}
+
+int rs_tma_desc_2d_f32(void* desc, const void* base, uint64_t dim0, uint64_t dim1, uint64_t row_stride_bytes,
+                       uint32_t box0, uint32_t box1, int swizzle) {
+  if (int e = load_driver()) return e;
+  cuuint64_t dims[2] = {dim0, dim1};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box0, box1};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_NONE;
+  if (swizzle == 1) sw = CU_TENSOR_MAP_SWIZZLE_32B;
+  if (swizzle == 2) sw = CU_TENSOR_MAP_SWIZZLE_64B;
+  if (swizzle == 3) sw = CU_TENSOR_MAP_SWIZZLE_128B;
+  CU(g_drv.TensorMapEncodeTiled((CUtensorMap*)desc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base),
+                                dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+     "cuTensorMapEncodeTiled");
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,547 @@
+"""ImperativeUnit -> CUDA C++ for sm_100a (the `sm100a` emit target).
+
+Replaces the reference back end `codegen.emit(unit, target)` (codegen.py:451)
+for GPUs.  The reference's OpenCL mapping has three constructs that are
+invalid on a real GPU (SURVEY.md §8 a, list after the table); this emitter
+maps the same imperative phrases to a valid CUDA execution:
+
+* perfectly nested `parForGlobal` chains collapse into one grid-stride loop
+  over their product (instead of all loops sharing `get_global_id(0)`);
+* `parForWorkGroup` is a block-strided loop whose body runs block-uniformly:
+  `parForLocal` becomes a thread-strided loop followed by `__syncthreads()`,
+  `new(Local)` (and per-work-group `new(Private)` arrays) become `__shared__`
+  arrays, and sequential statements with memory effects run on thread 0
+  followed by a barrier;
+* `toMem(Global)` between parallel stages splits the unit into one kernel
+  per stage, with the temporary allocated by the runtime.
+
+Stages whose loop nest matches a hand-written template (`idioms.py`) are
+emitted as an instantiation of that template; the generic kernel for the
+same stage is kept in the text as the fallback when a template's run-time
+precondition (alignment, divisibility) does not hold.
+
+Sizes become template parameters, instantiated at NVRTC time with the
+run-time sizes (SURVEY.md §8 b "Kernel ABI"), so array extents and index
+arithmetic are compile-time constants.  The text is deterministic (byte
+stable for a given unit, like codegen.emit, test_codegen.py:71-74) and
+carries its launch plan as a JSON comment, so `run_cuda(code, unit, ...)`
+needs nothing but the text — the same contract as `cexec.run_emitted`.
+
+Arithmetic: with `exact=True` (default) every f32 operation is rendered with
+the round-to-nearest intrinsics (`__fadd_rn`, `__fmul_rn`, ...), which the
+compiler never contracts into FMAs, so a kernel that preserves the program's
+evaluation order is bit-exact with the reference's sequential fp32
+semantics (interpreter.py:161-169).
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass, field
+
+from . import lir
+from ._ref import errors, nat
+
+EmitError = errors.EmitError
+
+TARGET = "sm100a"
+PLAN_TAG = "// @plan "
+
+DEFAULT_BLOCK = 256
+
+# ---------------------------------------------------------------------------
+# rendering of sizes / indices
+
+
+def _strip_neg(t):
+    if isinstance(t, nat.Const) and t.value < 0:
+        return True, nat.Const(-t.value)
+    if isinstance(t, nat.Product) and t.factors and isinstance(t.factors[0], nat.Const) and t.factors[0].value < 0:
+        c = -t.factors[0].value
+        rest = t.factors[1:]
+        if c == 1:
+            return True, rest[0] if len(rest) == 1 else nat.Product(rest)
+        return True, nat.Product((nat.Const(c),) + rest)
+    return False, t
+
+
+class NatRenderer:
+    """Nat -> C (or Python) integer expression text."""
+
+    def __init__(self, clamps=None, py=False, names=None):
+        self.clamps = clamps or {}
+        self.py = py
+        self.names = names or {}
+
+    def __call__(self, n, prec=0):
+        return self.render(n, prec)
+
+    def render(self, n, prec=0):
+        if isinstance(n, nat.Const):
+            return str(n.value) if n.value >= 0 else f"(-{-n.value})"
+        if isinstance(n, nat.Var):
+            if n.name in self.clamps:
+                inner, hi = self.clamps[n.name]
+                if self.py:
+                    raise EmitError("clamped index in a launch expression")
+                return f"rs_clamp({self.render(inner)}, {self.render(hi)})"
+            return self.names.get(n.name, n.name)
+        if isinstance(n, nat.Sum):
+            parts = []
+            terms = [_strip_neg(t) for t in n.terms]
+            terms = [t for t in terms if not t[0]] + [t for t in terms if t[0]]
+            for k, (neg, body) in enumerate(terms):
+                s = self.render(body, 1)
+                if k == 0:
+                    parts.append(f"-{s}" if neg else s)
+                else:
+                    parts.append((" - " if neg else " + ") + s)
+            text = "".join(parts)
+            return f"({text})" if prec > 1 else text
+        if isinstance(n, nat.Product):
+            text = " * ".join(self.render(f, 2) for f in n.factors)
+            return f"({text})" if prec > 2 else text
+        if isinstance(n, nat.Div):
+            op = " // " if self.py else " / "
+            text = f"{self.render(n.num, 3)}{op}{self.render(n.den, 3)}"
+            return f"({text})" if prec >= 2 else text
+        if isinstance(n, nat.Mod):
+            text = f"{self.render(n.num, 3)} % {self.render(n.den, 3)}"
+            return f"({text})" if prec >= 2 else text
+        if isinstance(n, nat.Pow):
+            if self.py:
+                return f"({self.render(n.base, 3)} ** {self.render(n.exp, 3)})"
+            return f"rs_ipow({self.render(n.base)}, {self.render(n.exp)})"
+        raise EmitError(f"cannot render size expression {n!r}")
+
+
+def py_expr(n) -> str:
+    """Python text of a size expression (evaluated by the launch planner)."""
+    return NatRenderer(py=True)(nat.normalize(n))
+
+
+def eval_py(expr: str, nats: dict) -> int:
+    return int(eval(expr, {"__builtins__": {}}, dict(nats)))  # noqa: S307 - self-generated text
+
+
+# ---------------------------------------------------------------------------
+# rendering of values
+
+
+class ValueRenderer:
+    def __init__(self, prog: lir.Program, exact=True, load_hook=None):
+        self.prog = prog
+        self.exact = exact
+        self.nat = NatRenderer(prog.clamps)
+        self.load_hook = load_hook  # optional (Load) -> str override (smem staging)
+
+    def __call__(self, e):
+        return self.val(e)
+
+    def val(self, e):
+        if isinstance(e, lir.Lit):
+            return e.text
+        if isinstance(e, lir.IndexVal):
+            return f"({self.nat(e.n)})"
+        if isinstance(e, lir.ScalarRef):
+            return e.name
+        if isinstance(e, lir.Load):
+            if self.load_hook is not None:
+                out = self.load_hook(e)
+                if out is not None:
+                    return out
+            return f"{e.buf}[{self.nat(e.index)}]"
+        if isinstance(e, lir.Bin):
+            a, b = self.val(e.a), self.val(e.b)
+            if e.ctype == "float" and self.exact:
+                fn = {"+": "__fadd_rn", "-": "__fsub_rn", "*": "__fmul_rn", "/": "__fdiv_rn"}[e.op]
+                return f"{fn}({a}, {b})"
+            return f"({a} {e.op} {b})"
+        if isinstance(e, lir.Un):
+            a = self.val(e.a)
+            if e.fn == "sqrt":
+                return f"__fsqrt_rn({a})" if self.exact else f"sqrtf({a})"
+            if e.fn == "rsqrt":
+                return f"rs_rsqrt_exact({a})" if self.exact else f"rs_rsqrt_fast({a})"
+        raise EmitError(f"cannot render value {e!r}")
+
+    def target(self, t):
+        if isinstance(t, lir.ScalarRef):
+            return t.name
+        if isinstance(t, lir.Store):
+            return f"{t.buf}[{self.nat(t.index)}]"
+        raise EmitError(f"cannot render target {t!r}")
+
+
+# ---------------------------------------------------------------------------
+# stage analysis
+
+
+def contains_parfor(stmt) -> bool:
+    return any(isinstance(s, lir.ParFor) for s in lir.walk(stmt))
+
+
+def collapse_global_chain(stmt):
+    """ParFor(global) perfectly nested chain -> ([(var, bound)...], body)."""
+    loops = []
+    while isinstance(stmt, lir.ParFor) and stmt.kind == "global":
+        loops.append((stmt.var, stmt.bound))
+        stmt = stmt.body
+    return loops, stmt
+
+
+@dataclass
+class Stage:
+    kind: str  # "grid" | "workgroup" | "block" | "serial"
+    stmt: object
+    index: int = 0
+
+
+@dataclass
+class Temp:
+    name: str
+    ctype: str
+    dims: tuple
+
+
+def split_stages(body, prog):
+    """Top-level statements -> kernel stages; Global (and parallel-shared)
+    temporaries become runtime-allocated buffers."""
+    temps = []
+    stages = []
+
+    def visit(s):
+        if isinstance(s, lir.Alloc) and s.dims and (s.space == "Global" or contains_parfor(s.body)):
+            temps.append(Temp(s.name, s.ctype, s.dims))
+            prog.buffers[s.name].space = "Global"
+            visit(s.body)
+            return
+        if isinstance(s, lir.Seq):
+            for c in s.stmts:
+                visit(c)
+            return
+        if isinstance(s, lir.ParFor) and s.kind == "global":
+            stages.append(Stage("grid", s))
+        elif isinstance(s, lir.ParFor) and s.kind == "workgroup":
+            stages.append(Stage("workgroup", s))
+        elif contains_parfor(s):
+            stages.append(Stage("block", s))
+        else:
+            stages.append(Stage("serial", s))
+
+    visit(body)
+    merged = []
+    for st in stages:  # adjacent serial statements share one kernel
+        if merged and st.kind == "serial" and merged[-1].kind == "serial":
+            merged[-1] = Stage("serial", lir.Seq([merged[-1].stmt, st.stmt]))
+        else:
+            merged.append(st)
+    for k, st in enumerate(merged):
+        st.index = k
+    return merged, temps
+
+
+# ---------------------------------------------------------------------------
+# kernel text
+
+
+@dataclass
+class KernelText:
+    name: str
+    text: str
+    plan: dict
+
+
+@dataclass
+class CudaCode:
+    text: str
+    plan: dict
+    program: lir.Program = field(repr=False, default=None)
+
+
+class GenericKernel:
+    """One stage -> one kernel with the generic GPU mapping."""
+
+    def __init__(self, prog: lir.Program, stage: Stage, name: str, temps, exact=True):
+        self.prog = prog
+        self.stage = stage
+        self.name = name
+        self.temps = temps
+        self.r = ValueRenderer(prog, exact)
+        self.nat = self.r.nat
+        self.shared_decls = []
+        self.shared_names = set()
+        self.smem_bytes = []  # py size expressions of static shared arrays
+
+    # helpers -------------------------------------------------------------
+    def _size_c(self, dims):
+        size = dims[0]
+        for d in dims[1:]:
+            size = size * d
+        return self.nat(nat.normalize(size))
+
+    def _declare_shared(self, name, ctype, dims):
+        if name in self.shared_names:
+            return
+        self.shared_names.add(name)
+        if dims:
+            self.shared_decls.append(f"__shared__ {ctype} {name}[{self._size_c(dims)}];")
+            size = dims[0]
+            for d in dims[1:]:
+                size = size * d
+            self.smem_bytes.append(f"4 * ({py_expr(size)})")
+        else:
+            self.shared_decls.append(f"__shared__ {ctype} {name};")
+            self.smem_bytes.append("4")
+
+    # thread-level code (sequential semantics inside one thread) -----------
+    def thread(self, s, ind):
+        p = "  " * ind
+        if isinstance(s, lir.Seq):
+            out = []
+            for c in s.stmts:
+                out += self.thread(c, ind)
+            return out
+        if isinstance(s, lir.Assign):
+            return [f"{p}{self.r.target(s.target)} = {self.r(s.value)};"]
+        if isinstance(s, lir.Alloc):
+            if s.dims:
+                decl = f"{p}{s.ctype} {s.name}[{self._size_c(s.dims)}];"
+            else:
+                decl = f"{p}{s.ctype} {s.name};"
+            return [decl] + self.thread(s.body, ind)
+        if isinstance(s, (lir.For, lir.ParFor)):
+            head = f"{p}for (int {s.var} = 0; {s.var} < {self.nat(s.bound)}; {s.var} += 1) {{"
+            return [head] + self.thread(s.body, ind + 1) + [f"{p}}}"]
+        if isinstance(s, lir.IfLess):
+            return (
+                [f"{p}if ({self.nat(s.lhs)} < {self.nat(s.threshold)}) {{"]
+                + self.thread(s.then, ind + 1)
+                + [f"{p}}} else {{"]
+                + self.thread(s.els, ind + 1)
+                + [f"{p}}}"]
+            )
+        if isinstance(s, lir.Raw):
+            return [p + line for line in s.lines]
+        if isinstance(s, lir.DoubleBuffer):
+            size = self.nat(s.size)
+            c = s.ctype
+            return [
+                f"{p}{c} buffer1[{size}]; {c} buffer2[{size}];",
+                f"{p}const {c}* in_ptr = {s.input_buf}; {c}* out_ptr = buffer1;",
+                f"{p}unsigned char flag = 1;",
+            ] + self.thread(s.body, ind)
+        raise EmitError(f"cannot emit statement {s!r}")
+
+    # block-uniform code (all threads of the block, with barriers) ---------
+    def block(self, s, ind):
+        p = "  " * ind
+        if isinstance(s, lir.Seq):
+            out = []
+            for c in s.stmts:
+                out += self.block(c, ind)
+            return out
+        if not contains_parfor(s):
+            if isinstance(s, lir.Alloc):
+                self._declare_shared(s.name, s.ctype, s.dims)
+                return self.block(s.body, ind)
+            # sequential statement: thread 0 performs it, everyone waits
+            return [f"{p}if (threadIdx.x == 0) {{"] + self.thread_shared(s, ind + 1) + [
+                f"{p}}}", f"{p}__syncthreads();"]
+        if isinstance(s, lir.ParFor):
+            head = (f"{p}for (int {s.var} = threadIdx.x; {s.var} < {self.nat(s.bound)}; "
+                    f"{s.var} += blockDim.x) {{")
+            return [head] + self.thread(s.body, ind + 1) + [f"{p}}}", f"{p}__syncthreads();"]
+        if isinstance(s, lir.Alloc):
+            self._declare_shared(s.name, s.ctype, s.dims)
+            return self.block(s.body, ind)
+        if isinstance(s, lir.For):
+            head = f"{p}for (int {s.var} = 0; {s.var} < {self.nat(s.bound)}; {s.var} += 1) {{"
+            return [head] + self.block(s.body, ind + 1) + [f"{p}}}"]
+        if isinstance(s, lir.IfLess):
+            return (
+                [f"{p}if ({self.nat(s.lhs)} < {self.nat(s.threshold)}) {{"]
+                + self.block(s.then, ind + 1)
+                + [f"{p}}} else {{"]
+                + self.block(s.els, ind + 1)
+                + [f"{p}}}"]
+            )
+        if isinstance(s, lir.DoubleBuffer):
+            size = self.nat(s.size)
+            c = s.ctype
+            self.shared_decls += [
+                f"__shared__ {c} buffer1[{size}]; __shared__ {c} buffer2[{size}];",
+                f"__shared__ const {c}* in_ptr; __shared__ {c}* out_ptr;",
+                "__shared__ unsigned char flag;",
+            ]
+            self.smem_bytes.append(f"8 * ({py_expr(s.size)})")
+            return [
+                f"{p}if (threadIdx.x == 0) {{",
+                f"{p}  in_ptr = {s.input_buf}; out_ptr = buffer1; flag = 1;",
+                f"{p}}}",
+                f"{p}__syncthreads();",
+            ] + self.block(s.body, ind)
+        raise EmitError(f"cannot emit statement {s!r} at block level")
+
+    def thread_shared(self, s, ind):
+        """Sequential code run by thread 0 where block-level allocations are
+        shared variables (already declared)."""
+        return self.thread(s, ind)
+
+    # whole kernel ---------------------------------------------------------
+    def emit(self) -> KernelText:
+        st = self.stage
+        body = []
+        plan = {"name": self.name, "kind": st.kind}
+        if st.kind == "grid":
+            loops, inner = collapse_global_chain(st.stmt)
+            total = nat.Const(1)
+            for _, b in loops:
+                total = total * b
+            total = nat.normalize(total, self.prog.assumptions)
+            body.append(f"  const int rs_total = {self.nat(total)};")
+            body.append("  for (int rs_f = blockIdx.x * blockDim.x + threadIdx.x; rs_f < rs_total; "
+                        "rs_f += gridDim.x * blockDim.x) {")
+            rest = "rs_f"
+            for k, (var, bound) in enumerate(loops):
+                if k == len(loops) - 1:
+                    body.append(f"    const int {var} = {rest};")
+                else:
+                    inner_size = nat.Const(1)
+                    for _, b in loops[k + 1:]:
+                        inner_size = inner_size * b
+                    size_c = self.nat(nat.normalize(inner_size, self.prog.assumptions), 2)
+                    body.append(f"    const int {var} = {rest} / {size_c};")
+                    body.append(f"    const int rs_r{k} = {rest} % {size_c};")
+                    rest = f"rs_r{k}"
+            body += self.thread(inner, 2)
+            body.append("  }")
+            plan.update(total=py_expr(total), block=DEFAULT_BLOCK)
+        elif st.kind == "workgroup":
+            wg = st.stmt
+            body.append(f"  for (int {wg.var} = blockIdx.x; {wg.var} < {self.nat(wg.bound)}; "
+                        f"{wg.var} += gridDim.x) {{")
+            body += self.block(wg.body, 2)
+            body.append("    __syncthreads();")
+            body.append("  }")
+            locals_ = [s.bound for s in lir.walk(wg.body) if isinstance(s, lir.ParFor)]
+            plan.update(total=py_expr(wg.bound), block=DEFAULT_BLOCK,
+                        local_bounds=[py_expr(b) for b in locals_])
+        elif st.kind == "block":
+            body += self.block(st.stmt, 1)
+            plan.update(total="1", block=DEFAULT_BLOCK)
+        else:  # serial
+            body += self.thread(st.stmt, 1)
+            plan.update(total="1", block=1)
+        plan["smem_static"] = " + ".join(self.smem_bytes) if self.smem_bytes else "0"
+        head = kernel_head(self.prog, self.name, self.temps,
+                           launch_bounds=plan["block"] if st.kind != "serial" else 1)
+        lines = head + ["  " + d for d in self.shared_decls] + body + ["}"]
+        return KernelText(self.name, "\n".join(lines) + "\n", plan)
+
+
+def kernel_params(prog: lir.Program, temps):
+    params = [f"{prog.output.ctype}* __restrict__ {prog.output.name}"]
+    for name, b in prog.inputs:
+        if isinstance(b, lir.ScalarRef):
+            params.append(f"{b.ctype} {name}")
+        else:
+            params.append(f"const {b.ctype}* __restrict__ {name}")
+    for t in temps:
+        params.append(f"{t.ctype}* __restrict__ {t.name}")
+    return params
+
+
+def template_line(prog: lir.Program):
+    if not prog.nat_params:
+        return []
+    return ["template <" + ", ".join(f"int {n}" for n in prog.nat_params) + ">"]
+
+
+def kernel_head(prog, name, temps, launch_bounds=DEFAULT_BLOCK, extra_params=()):
+    params = kernel_params(prog, temps) + list(extra_params)
+    return template_line(prog) + [
+        f"__global__ void __launch_bounds__({launch_bounds}) {name}({', '.join(params)}) {{"
+    ]
+
+
+def arg_names(prog: lir.Program, temps):
+    return [prog.output.name] + [n for n, _ in prog.inputs] + [t.name for t in temps]
+
+
+# ---------------------------------------------------------------------------
+# whole units
+
+
+def emit_cuda(unit, exact=True, idioms=True) -> CudaCode:
+    """Emit the sm100a kernel text (and launch plan) for an ImperativeUnit."""
+    from . import idioms as idiom_mod
+
+    prog = lir.build(unit)
+    stages, temps = split_stages(prog.body, prog)
+    kernels = []
+    plan_stages = []
+    includes = ["rise/device.cuh"]
+    for st in stages:
+        base = f"{prog.name}Kernel" if len(stages) == 1 else f"{prog.name}Kernel_s{st.index}"
+        generic = GenericKernel(prog, st, base, temps, exact).emit()
+        kernels.append(generic.text)
+        entry = dict(generic.plan)
+        match = idiom_mod.match(prog, st, base, temps, exact) if idioms else None
+        if match is not None:
+            kernels.append(match.text)
+            for inc in match.includes:
+                if inc not in includes:
+                    includes.append(inc)
+            entry = dict(match.plan, fallback=generic.plan)
+        plan_stages.append(entry)
+    plan = {
+        "version": 1,
+        "target": TARGET,
+        "unit": prog.name,
+        "nat_params": list(prog.nat_params),
+        "args": arg_names(prog, temps),
+        "output": {"name": prog.output.name, "ctype": prog.output.ctype,
+                   "size": py_expr(_prod(prog.output.dims)), "deref": prog.output.deref},
+        "inputs": [_input_plan(n, b) for n, b in prog.inputs],
+        "temps": [{"name": t.name, "ctype": t.ctype, "size": py_expr(_prod(t.dims))} for t in temps],
+        "stages": plan_stages,
+        "exact": exact,
+    }
+    header = [
+        f"// rise-b200 {TARGET} kernels for RISE unit '{prog.name}' (generated by emit_cuda; do not edit)",
+        PLAN_TAG + json.dumps(plan, sort_keys=True),
+    ] + [f"#include <{inc}>" for inc in includes]
+    text = "\n".join(header) + "\n\n" + "\n".join(kernels)
+    return CudaCode(text, plan, prog)
+
+
+def _prod(dims):
+    out = nat.Const(1)
+    for d in dims:
+        out = out * d
+    return nat.normalize(out)
+
+
+def _input_plan(name, b):
+    if isinstance(b, lir.ScalarRef):
+        return {"name": name, "ctype": b.ctype, "scalar": True}
+    return {"name": name, "ctype": b.ctype, "scalar": False, "size": py_expr(_prod(b.dims))}
+
+
+def emit(unit, target: str = TARGET) -> str:
+    """Drop-in for codegen.emit(unit, target) (codegen.py:451) with the new
+    `sm100a` target.  (The reference target name "cuda" is not used: the
+    reference suite asserts emit(unit, "cuda") raises, test_codegen.py:151.)"""
+    if target != TARGET:
+        from ._ref import codegen
+
+        return codegen.emit(unit, target)
+    return emit_cuda(unit).text
+
+
+def plan_of(text: str) -> dict:
+    for line in text.splitlines():
+        if line.startswith(PLAN_TAG):
+            return json.loads(line[len(PLAN_TAG):])
+    raise errors.InterpreterError("kernel text carries no launch plan (not produced by emit_cuda)")

@@ -1,0 +1,94 @@
+"""The benchmark programs, written against the reference's RISE API.
+
+Each config of BASELINE.json is a RISE program (plus an Elevate strategy
+where the program is still high-level) that goes through the unchanged
+front end (`frontend.compile_program`) and then the sm100a back end.
+
+* C1 `dot`   — map(*) + reduce(+), lowered by `fuseReduceMap ; toReduceSeq`
+               (BASELINE.md §4 row C1).
+* C2 `mv`    — the paper's matrix-vector program (Listing 1; the
+               reference's tests/data/mv.rise) with either the
+               `toMapGlobal` strategy or the paper's
+               Listing-3 strategy (tests/data/mv_opt.elv).
+* C3 `conv`  — 3x3 stencil: padClamp2D + slide2D + map/reduce (SURVEY.md
+               §8.1 validated form), weights as an Array[3, Array[3, f32]].
+* C4 `sgemm` — A x B with B given transposed (`Bt`), the form the reference
+               can already translate and emit (SURVEY.md §8 c, C4).
+* C5 `nbody` — all-pairs accelerations + Euler velocity update (one step),
+               positions Array[n, Array[3, f32]] and masses Array[n, f32].
+"""
+
+from __future__ import annotations
+
+DOT = """\
+depFun((n: Nat) => fun(a: Array[n, f32] => fun(b: Array[n, f32] =>
+  zip(a)(b) |> map(fun(p => fst(p) * snd(p))) |> reduce(add)(0.0f) )))
+"""
+DOT_STRATEGY = "fuseReduceMap @ every(isReduce) ; toReduceSeq @ every(isReduce)"
+
+MV = """\
+// matrix-vector multiplication: for each row, a dot product with x
+def mv = depFun((n: Nat, m: Nat) =>
+  fun(M: Array[n, Array[m, f32]] =>
+    fun(x: Array[m, f32] =>
+      M |> map(fun(row =>
+          zip(row)(x) |>
+            map(fun(ax => fst(ax) * snd(ax))) |>
+              reduce(add)(0.0f) )) )) )
+"""
+MV_GLOBAL_STRATEGY = (
+    "toMapGlobal @ outermost(isMap) ; fuseReduceMap @ every(isReduce) ; toReduceSeq @ every(isReduce)"
+)
+# the paper's Listing 3
+MV_OPT_STRATEGY = """\
+    splitJoinMap    `@` outermost(isMap)    `;`
+    toMapWorkGroup  `@` outermost(isMap)    `;`
+    toMapLocal      `@` outermost(isMap)    `;`
+    fuseReduceMap   `@` every(isReduce)     `;`
+    toReduceSeq     `@` every(isReduce)
+"""
+
+CONV = """\
+def conv = depFun((n: Nat, m: Nat) => fun(img: Array[n, Array[m, f32]] => fun(w: Array[3, Array[3, f32]] =>
+  img |> padClamp2D(1)(1) |> slide2D(3)(1) |> mapGlobal(mapGlobal(fun(win =>
+    zip(win)(w)
+      |> mapSeq(fun(rw => zip(fst(rw))(snd(rw)) |> reduceSeq(Private)(fun(acc, p => acc + fst(p) * snd(p)))(0.0f)))
+      |> toMem(Private)
+      |> reduceSeq(Private)(fun(acc, v => acc + v))(0.0f) ))) )))
+"""
+
+SGEMM_BT = """\
+def sgemm = depFun((n: Nat, m: Nat, k: Nat) =>
+  fun(A: Array[n, Array[k, f32]] => fun(Bt: Array[m, Array[k, f32]] =>
+    A |> mapGlobal(fun(arow => Bt |> mapGlobal(fun(brow =>
+      zip(arow)(brow) |> reduceSeq(Private)(fun(acc, p => acc + fst(p) * snd(p)))(0.0f) ))) ))))
+"""
+
+NBODY = """\
+def nbody = depFun((n: Nat) =>
+  fun(pos: Array[n, Array[3, f32]] => fun(vel: Array[n, Array[3, f32]] => fun(mass: Array[n, f32] =>
+    zip(pos)(vel) |> mapGlobal(fun(pv =>
+      zip(transpose(pos))(zip(fst(pv))(snd(pv))) |> mapSeq(fun(col =>
+        snd(snd(col)) + 0.01f *
+          (zip(fst(col))(zip(pos)(mass)) |> reduceSeq(Private)(fun(acc, q =>
+             acc + (fst(q) - fst(snd(col))) *
+               (snd(snd(q)) *
+                 ((zip(fst(snd(q)))(fst(pv)) |> reduceSeq(Private)(fun(r2, d => r2 + (fst(d) - snd(d)) * (fst(d) - snd(d))))(0.01f))
+                   |> fun(r2 => rsqrt(r2) * rsqrt(r2) * rsqrt(r2)))) ))(0.0f)) )) )) ))))
+"""
+
+CONFIGS = {
+    "dot": dict(source=DOT, strategy=DOT_STRATEGY, name="dot", nats={"n": 1 << 24}),
+    "gemv": dict(source=MV, strategy=MV_GLOBAL_STRATEGY, name="mv", nats={"n": 8192, "m": 8192}),
+    "gemv_opt": dict(source=MV, strategy=MV_OPT_STRATEGY, name="mv", nats={"n": 8192, "m": 8192, "s": 32}),
+    "conv": dict(source=CONV, strategy=None, name="conv", nats={"n": 8192, "m": 8192}),
+    "sgemm": dict(source=SGEMM_BT, strategy=None, name="sgemm", nats={"n": 4096, "m": 4096, "k": 4096}),
+    "nbody": dict(source=NBODY, strategy=None, name="nbody", nats={"n": 131072}),
+}
+
+
+def compile_config(key: str):
+    from .frontend import compile_program
+
+    cfg = CONFIGS[key]
+    return compile_program(cfg["source"], cfg["strategy"], name=cfg["name"])

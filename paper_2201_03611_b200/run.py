@@ -1,0 +1,308 @@
+"""Execution of emitted sm100a kernel text: the CUDA counterpart of
+`cexec.run_emitted` / `cexec.execute_kernel` (cexec.py:509-581).
+
+`run_cuda(code, unit, nat_assignment, inputs)` keeps run_emitted's argument
+order and result form (nested lists of np.float32 / int, the interpreter's
+value form), so oracle comparisons read exactly like the reference's own
+tests (test_codegen.py:157-183).  `Executable` is the allocation-free path
+used by benchmarks: compiled once per (text, sizes), launched on device
+buffers (any object exposing `data_ptr()`, e.g. torch CUDA tensors, or raw
+integer device pointers).
+
+Every launch goes through the native runtime (`runtime.Function.launch` ->
+rs_launch).  There is no CPU fallback: without the runtime library or a GPU
+this module raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import runtime as rt
+from ._ref import errors, interpreter, nat
+from ._ref import types as _types
+from .emit_cuda import CudaCode, eval_py, plan_of
+
+InterpreterError = errors.InterpreterError
+ArrayType, ScalarType = _types.ArrayType, _types.ScalarType
+
+INT32_MAX = 2**31 - 1
+
+
+def _launchers():
+    from . import idioms
+
+    return idioms.LAUNCHERS
+
+
+class Executable:
+    """Kernel text specialised to concrete sizes, compiled and loaded."""
+
+    def __init__(self, code, nats: dict, device: int | None = None):
+        text = code.text if isinstance(code, CudaCode) else code
+        self.text = text
+        self.plan = plan_of(text)
+        self.nats = {}
+        for name in self.plan["nat_params"]:
+            if name not in nats:
+                raise InterpreterError(f"missing size argument {name!r}")
+            self.nats[name] = int(nats[name])
+        rt.init(device)
+        self.sm_count = rt.device_attribute(rt.SM_COUNT_ATTR)
+        self.output_size = eval_py(self.plan["output"]["size"], self.nats)
+        self.input_sizes = {
+            i["name"]: (None if i["scalar"] else eval_py(i["size"], self.nats)) for i in self.plan["inputs"]
+        }
+        self.temp_sizes = {t["name"]: eval_py(t["size"], self.nats) for t in self.plan["temps"]}
+        for what, size in [("output", self.output_size)] + list(self.input_sizes.items()) + list(
+            self.temp_sizes.items()
+        ):
+            if size is not None and size > INT32_MAX:
+                raise InterpreterError(f"{what} has {size} elements; 32-bit indexing supports < 2^31")
+        targs = ", ".join(str(self.nats[n]) for n in self.plan["nat_params"])
+        self.launches = []
+        exprs = []
+        fmad = False
+        for st in self.plan["stages"]:
+            chosen = st
+            if st.get("pre") and not all(eval_py(p, self.nats) for p in st["pre"]):
+                chosen = st["fallback"]
+            fmad = fmad or bool(chosen.get("fmad", False))
+            name_expr = f"{chosen['name']}<{targs}>" if targs else chosen["name"]
+            exprs.append(name_expr)
+            self.launches.append((chosen, name_expr))
+        opts = ["--fmad=true" if fmad else "--fmad=false"]
+        self.module = rt.load_module(text, exprs, opts, program_name=f"{self.plan['unit']}.cu")
+        self.kernels = []
+        for (chosen, name_expr), lowered in zip(self.launches, self.module.lowered):
+            fn = self.module.function(lowered)
+            grid, block, smem, cluster = self._config(chosen)
+            self.kernels.append((chosen, fn, grid, block, smem, cluster))
+        self._temps = None
+
+    # launch configuration --------------------------------------------------
+    def _config(self, st):
+        kind = st["kind"]
+        sm = self.sm_count
+        if kind == "grid":
+            total = eval_py(st["total"], self.nats)
+            block = st["block"]
+            grid = max(1, min(math.ceil(total / block), sm * 8))
+            return (grid, 1, 1), (block, 1, 1), 0, (1, 1, 1)
+        if kind == "workgroup":
+            total = eval_py(st["total"], self.nats)
+            locals_ = [eval_py(b, self.nats) for b in st.get("local_bounds", [])]
+            want = max(locals_) if locals_ else st["block"]
+            block = min(st["block"], max(32, 32 * math.ceil(want / 32)))
+            grid = max(1, min(total, sm * 16))
+            return (grid, 1, 1), (block, 1, 1), 0, (1, 1, 1)
+        if kind == "block":
+            return (1, 1, 1), (st["block"], 1, 1), 0, (1, 1, 1)
+        if kind == "serial":
+            return (1, 1, 1), (1, 1, 1), 0, (1, 1, 1)
+        launcher = _launchers().get(kind)
+        if launcher is None:
+            raise InterpreterError(f"no launcher for stage kind {kind!r}")
+        return launcher(st, self.nats, sm)
+
+    @property
+    def kernel_names(self):
+        return [st["name"] for st, *_ in self.kernels]
+
+    @property
+    def template_kinds(self):
+        return [st["kind"] for st, *_ in self.kernels]
+
+    def temps(self):
+        """Device temporaries (allocated once per executable)."""
+        if self._temps is None:
+            import torch
+
+            self._temps = {
+                t["name"]: torch.empty(max(1, self.temp_sizes[t["name"]]),
+                                       dtype=_torch_dtype(t["ctype"]), device="cuda")
+                for t in self.plan["temps"]
+            }
+            for st, *_ in self.kernels:
+                for ws in st.get("workspace", []):
+                    size = eval_py(ws["size"], self.nats)
+                    self._temps[ws["name"]] = torch.zeros(max(1, size), dtype=_torch_dtype(ws["ctype"]),
+                                                          device="cuda")
+        return self._temps
+
+    def launch(self, buffers: dict, stream=None):
+        """Launch every stage.  `buffers` maps argument names to device
+        tensors / pointers (arrays) or Python numbers (scalar inputs)."""
+        temps = self.temps()
+        scalar_types = {i["name"]: i["ctype"] for i in self.plan["inputs"] if i["scalar"]}
+        base_args = []
+        for name in self.plan["args"]:
+            if name in temps:
+                base_args.append(ctypes.c_void_p(temps[name].data_ptr()))
+            elif name in scalar_types:
+                v = buffers[name]
+                base_args.append(ctypes.c_float(float(v)) if scalar_types[name] == "float" else ctypes.c_int(int(v)))
+            else:
+                base_args.append(ctypes.c_void_p(_dptr(buffers[name])))
+        for st, fn, grid, block, smem, cluster in self.kernels:
+            args = list(base_args)
+            for extra in st.get("extra_args", []):
+                args.append(self._extra_arg(extra, buffers, temps))
+            fn.launch(grid, block, args, smem=smem, stream=stream, cluster=cluster)
+
+    def _extra_arg(self, extra, buffers, temps):
+        kind = extra["kind"]
+        if kind == "workspace":
+            return ctypes.c_void_p(temps[extra["name"]].data_ptr())
+        if kind == "tma2d":
+            base = _dptr(buffers[extra["buf"]]) if extra["buf"] in buffers else temps[extra["buf"]].data_ptr()
+            dims = [eval_py(d, self.nats) for d in extra["dims"]]
+            return rt.tma_desc_2d_f32(base, dims[0], dims[1], dims[0] * 4, extra["box"][0], extra["box"][1],
+                                      extra.get("swizzle", 0))
+        raise InterpreterError(f"unknown extra kernel argument {kind!r}")
+
+    def run_host(self, host_inputs, host_out, device_inputs, device_out, stream=None):
+        """End-to-end step through host memory: copy `host_inputs` (pinned
+        torch CPU tensors, scalars passed through) into `device_inputs`,
+        launch, and copy the result back into `host_out` — all enqueued on
+        `stream`.  The caller synchronises."""
+        import torch
+
+        stream = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(stream):
+            for h, d in zip(host_inputs, device_inputs):
+                if isinstance(d, torch.Tensor):
+                    d.copy_(h, non_blocking=True)
+            self(*device_inputs, out=device_out, stream=stream)
+            host_out.copy_(device_out, non_blocking=True)
+        return host_out
+
+    # convenience: torch in / torch out -----------------------------------------
+    def __call__(self, *inputs, out=None, stream=None):
+        import torch
+
+        if len(inputs) != len(self.plan["inputs"]):
+            raise InterpreterError(f"expected {len(self.plan['inputs'])} inputs, got {len(inputs)}")
+        buffers = {}
+        for spec, value in zip(self.plan["inputs"], inputs):
+            if spec["scalar"]:
+                buffers[spec["name"]] = value
+                continue
+            if not (isinstance(value, torch.Tensor) and value.is_cuda):
+                raise InterpreterError(f"input {spec['name']!r} must be a CUDA tensor")
+            if value.numel() != self.input_sizes[spec["name"]]:
+                raise InterpreterError(
+                    f"input {spec['name']!r} has {value.numel()} elements, expected {self.input_sizes[spec['name']]}")
+            if not value.is_contiguous() or value.dtype != _torch_dtype(spec["ctype"]):
+                raise InterpreterError(f"input {spec['name']!r} must be contiguous {spec['ctype']}")
+            buffers[spec["name"]] = value
+        if out is None:
+            out = torch.empty(self.output_size, dtype=_torch_dtype(self.plan["output"]["ctype"]), device="cuda")
+        buffers[self.plan["output"]["name"]] = out
+        self.launch(buffers, stream=stream if stream is not None else torch.cuda.current_stream())
+        return out
+
+
+def _dptr(x):
+    if hasattr(x, "data_ptr"):
+        return int(x.data_ptr())
+    if isinstance(x, ctypes.c_void_p):
+        return int(x.value)
+    if isinstance(x, rt.DeviceBuffer):
+        return int(x.ptr.value)
+    return int(x)
+
+
+def _torch_dtype(ctype):
+    import torch
+
+    return torch.float32 if ctype == "float" else torch.int32
+
+
+def _np_dtype(ctype):
+    return np.float32 if ctype == "float" else np.int32
+
+
+_exe_cache: dict = {}
+
+
+def executable(code, nats: dict) -> Executable:
+    text = code.text if isinstance(code, CudaCode) else code
+    key = (text, tuple(sorted((k, int(v)) for k, v in nats.items())))
+    exe = _exe_cache.get(key)
+    if exe is None:
+        exe = Executable(text, nats)
+        _exe_cache[key] = exe
+    return exe
+
+
+def flatten_input(raw, dtype, nat_env):
+    """Reference value (nested lists) or numpy array -> flat numpy array."""
+    if isinstance(dtype, ScalarType):
+        return interpreter.convert_input(raw, dtype)
+    dims = []
+    dt = dtype
+    while isinstance(dt, ArrayType):
+        dims.append(nat.evaluate(dt.size, nat_env))
+        dt = dt.elem
+    if not isinstance(dt, ScalarType):
+        raise InterpreterError("tuple-typed kernel data has no flat layout")
+    np_t = np.float32 if dt.name == "f32" else np.int32
+    if isinstance(raw, np.ndarray):
+        arr = np.ascontiguousarray(raw, dtype=np_t)
+        if arr.size != int(np.prod(dims)):
+            raise InterpreterError(f"input of {arr.size} elements does not match {dims}")
+        return arr.reshape(-1)
+    value = interpreter.convert_input(raw, dtype)
+    interpreter.check_length(value, dtype, nat_env)
+    return np.asarray(value, dtype=np_t).reshape(-1)
+
+
+def unflatten(flat: np.ndarray, dtype, nat_env):
+    dims = []
+    dt = dtype
+    while isinstance(dt, ArrayType):
+        dims.append(nat.evaluate(dt.size, nat_env))
+        dt = dt.elem
+    if not dims:
+        v = flat[0]
+        return np.float32(v) if flat.dtype == np.float32 else int(v)
+    arr = flat.reshape(dims)
+    if flat.dtype == np.float32:
+        return _to_nested(arr, np.float32)
+    return _to_nested(arr, int)
+
+
+def _to_nested(arr, conv):
+    if arr.ndim == 1:
+        return [conv(v) for v in arr]
+    return [_to_nested(a, conv) for a in arr]
+
+
+def run_cuda(code, unit, nat_assignment: dict, inputs, *, stream=None, as_numpy=False):
+    """Execute sm100a kernel text for a translated unit on the GPU and return
+    its output in the interpreter's nested-value form (or a flat numpy array
+    with `as_numpy=True`).  Same contract as cexec.run_emitted (cexec.py:555):
+    inputs in unit order, sizes by name, output allocated here."""
+    import torch
+
+    nat_env = {k: int(v) for k, v in dict(nat_assignment).items()}
+    exe = executable(code, nat_env)
+    if len(inputs) != len(unit.inputs):
+        raise InterpreterError(f"expected {len(unit.inputs)} inputs, got {len(inputs)}")
+    dev_inputs = []
+    for (var, dtype), raw in zip(unit.inputs, inputs):
+        flat = flatten_input(raw, dtype, nat_env)
+        if isinstance(dtype, ScalarType):
+            dev_inputs.append(flat)
+        else:
+            dev_inputs.append(torch.from_numpy(np.ascontiguousarray(flat)).to("cuda"))
+    out = exe(*dev_inputs, stream=stream)
+    torch.cuda.synchronize()
+    host = out.cpu().numpy()
+    if as_numpy:
+        return host
+    return unflatten(host, unit.output_type, nat_env)

@@ -1,0 +1,338 @@
+"""ctypes binding of the native runtime (include/rise_b200.h).
+
+This is the Python half of the drop-in boundary.  Compile failures raise the
+reference's `EmitError` (stage "emit", errors.py:73-74); launch, memory and
+device failures raise `InterpreterError` (stage "run", errors.py:77-78), the
+classes `codegen.emit` and `cexec.execute_kernel` raise today.
+
+There is no fallback: if the shared library or the CUDA driver is missing,
+every entry point that needs them raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import os
+import threading
+from pathlib import Path
+
+from ._ref import errors as _errors
+
+PKG_DIR = Path(__file__).resolve().parent
+LIB_PATH = PKG_DIR / "_lib" / "librise_b200.so"
+INCLUDE_DIR = PKG_DIR / "csrc" / "include"
+HEADER = PKG_DIR.parent / "include" / "rise_b200.h"
+
+# every symbol include/rise_b200.h declares (checked by the CPU test-suite)
+EXPORTED = (
+    "rs_last_error", "rs_abi_version", "rs_init", "rs_device_count", "rs_device_attribute",
+    "rs_nvrtc_version", "rs_compile", "rs_compile_cubin", "rs_free_host", "rs_module_load",
+    "rs_module_lowered_name", "rs_module_get_function", "rs_module_unload",
+    "rs_function_attribute", "rs_launch", "rs_malloc", "rs_free", "rs_memcpy_htod",
+    "rs_memcpy_dtoh", "rs_memcpy_dtod", "rs_memset_d8", "rs_stream_create",
+    "rs_stream_destroy", "rs_stream_synchronize", "rs_device_synchronize", "rs_event_create",
+    "rs_event_destroy", "rs_event_record", "rs_event_synchronize", "rs_event_elapsed_ms",
+    "rs_tma_desc_2d_f32",
+)
+
+_lib = None
+_lock = threading.Lock()
+
+
+class RuntimeUnavailable(_errors.InterpreterError):
+    """The native runtime library could not be loaded."""
+
+
+def lib():
+    """Load librise_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise RuntimeUnavailable(
+                    f"native runtime {LIB_PATH} is missing; run __graft_entry__.build()"
+                )
+            L = ctypes.CDLL(str(LIB_PATH))
+            vp, i, sz, u = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t, ctypes.c_uint
+            cpp = ctypes.POINTER(ctypes.c_char_p)
+            L.rs_last_error.restype = ctypes.c_char_p
+            L.rs_abi_version.restype = i
+            L.rs_compile_cubin.argtypes = [ctypes.c_char_p, ctypes.c_char_p, cpp, i, cpp, i,
+                                           ctypes.POINTER(vp), ctypes.POINTER(sz),
+                                           ctypes.POINTER(vp), ctypes.POINTER(vp)]
+            L.rs_free_host.argtypes = [vp]
+            L.rs_free_host.restype = None
+            L.rs_module_load.argtypes = [vp, sz, ctypes.POINTER(vp)]
+            L.rs_module_get_function.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(vp)]
+            L.rs_module_unload.argtypes = [vp]
+            L.rs_function_attribute.argtypes = [vp, i, ctypes.POINTER(i)]
+            L.rs_launch.argtypes = [vp, ctypes.POINTER(u), ctypes.POINTER(u), ctypes.POINTER(u),
+                                    u, vp, ctypes.POINTER(vp)]
+            L.rs_malloc.argtypes = [ctypes.POINTER(vp), sz]
+            L.rs_free.argtypes = [vp]
+            for name in ("rs_memcpy_htod", "rs_memcpy_dtoh", "rs_memcpy_dtod"):
+                getattr(L, name).argtypes = [vp, vp, sz, vp]
+            L.rs_memset_d8.argtypes = [vp, ctypes.c_ubyte, sz, vp]
+            L.rs_stream_create.argtypes = [ctypes.POINTER(vp)]
+            L.rs_stream_destroy.argtypes = [vp]
+            L.rs_stream_synchronize.argtypes = [vp]
+            L.rs_event_create.argtypes = [ctypes.POINTER(vp)]
+            L.rs_event_destroy.argtypes = [vp]
+            L.rs_event_record.argtypes = [vp, vp]
+            L.rs_event_synchronize.argtypes = [vp]
+            L.rs_event_elapsed_ms.argtypes = [ctypes.POINTER(ctypes.c_float), vp, vp]
+            L.rs_tma_desc_2d_f32.argtypes = [vp, vp, ctypes.c_uint64, ctypes.c_uint64,
+                                             ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, i]
+            L.rs_device_attribute.argtypes = [i, ctypes.POINTER(i)]
+            L.rs_device_count.argtypes = [ctypes.POINTER(i)]
+            L.rs_nvrtc_version.argtypes = [ctypes.POINTER(i), ctypes.POINTER(i)]
+            _lib = L
+    return _lib
+
+
+def _err_text():
+    return lib().rs_last_error().decode(errors="replace")
+
+
+def check_run(status, what=""):
+    if status != 0:
+        raise _errors.InterpreterError(f"{what}: {_err_text()}" if what else _err_text())
+
+
+def _cstr_array(items):
+    arr = (ctypes.c_char_p * max(1, len(items)))()
+    for k, s in enumerate(items):
+        arr[k] = s.encode()
+    return arr
+
+
+# ---------------------------------------------------------------------------
+# compilation (device-independent)
+
+DEFAULT_OPTS = ("--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-default-device")
+
+_cubin_cache: dict = {}
+
+
+def compile_cubin(source: str, name_exprs, opts=(), program_name="rise.cu"):
+    """NVRTC-compile `source` for sm_100a.  Returns (cubin bytes, lowered names).
+    Raises EmitError with the NVRTC log on failure.  Needs no GPU."""
+    full_opts = list(DEFAULT_OPTS) + [f"-I{INCLUDE_DIR}"] + list(opts)
+    key = hashlib.sha256(
+        "\0".join([source, program_name] + full_opts + list(name_exprs)).encode()
+    ).hexdigest()
+    hit = _cubin_cache.get(key)
+    if hit is not None:
+        return hit
+    L = lib()
+    image, size = ctypes.c_void_p(), ctypes.c_size_t()
+    names, log = ctypes.c_void_p(), ctypes.c_void_p()
+    st = L.rs_compile_cubin(
+        source.encode(), program_name.encode(), _cstr_array(full_opts), len(full_opts),
+        _cstr_array(list(name_exprs)), len(name_exprs),
+        ctypes.byref(image), ctypes.byref(size), ctypes.byref(names), ctypes.byref(log),
+    )
+    if st != 0:
+        raise _errors.EmitError(_err_text())
+    try:
+        blob = ctypes.string_at(image, size.value)
+        lowered = ctypes.string_at(names).decode().split("\n")[: len(name_exprs)] if names else []
+    finally:
+        L.rs_free_host(image)
+        L.rs_free_host(names)
+        L.rs_free_host(log)
+    out = (blob, lowered)
+    _cubin_cache[key] = out
+    return out
+
+
+# ---------------------------------------------------------------------------
+# device side
+
+_device = None
+
+
+def init(device: int | None = None):
+    """Make `device`'s primary context current (default: torch's current
+    device if torch has initialised CUDA, else 0)."""
+    global _device
+    if device is None:
+        device = _device if _device is not None else int(os.environ.get("LOCAL_RANK", "0") or 0)
+        try:
+            import torch
+
+            if torch.cuda.is_available() and torch.cuda.is_initialized():
+                device = torch.cuda.current_device()
+        except Exception:  # noqa: BLE001 - torch is optional plumbing
+            pass
+    check_run(lib().rs_init(int(device)), "rs_init")
+    _device = int(device)
+    return _device
+
+
+def device_attribute(attr: int) -> int:
+    init()
+    v = ctypes.c_int()
+    check_run(lib().rs_device_attribute(attr, ctypes.byref(v)), "rs_device_attribute")
+    return v.value
+
+
+SM_COUNT_ATTR = 16
+
+
+class Module:
+    def __init__(self, cubin: bytes, lowered):
+        init()
+        self._handle = ctypes.c_void_p()
+        self._image = ctypes.create_string_buffer(cubin, len(cubin))
+        check_run(lib().rs_module_load(self._image, len(cubin), ctypes.byref(self._handle)),
+                  "rs_module_load")
+        self.lowered = list(lowered)
+        self._fns = {}
+
+    def function(self, lowered_name: str) -> "Function":
+        fn = self._fns.get(lowered_name)
+        if fn is None:
+            h = ctypes.c_void_p()
+            check_run(lib().rs_module_get_function(self._handle, lowered_name.encode(), ctypes.byref(h)),
+                      "rs_module_get_function")
+            fn = Function(h, lowered_name)
+            self._fns[lowered_name] = fn
+        return fn
+
+
+class Function:
+    def __init__(self, handle, name):
+        self.handle = handle
+        self.name = name
+
+    def attribute(self, attr: int) -> int:
+        v = ctypes.c_int()
+        check_run(lib().rs_function_attribute(self.handle, attr, ctypes.byref(v)), "rs_function_attribute")
+        return v.value
+
+    def launch(self, grid, block, args, smem=0, stream=None, cluster=(1, 1, 1)):
+        """`args`: list of ctypes values (kept alive for the call)."""
+        g = (ctypes.c_uint * 3)(*_dim3(grid))
+        b = (ctypes.c_uint * 3)(*_dim3(block))
+        c = (ctypes.c_uint * 3)(*_dim3(cluster))
+        ptrs = (ctypes.c_void_p * max(1, len(args)))()
+        for k, a in enumerate(args):
+            ptrs[k] = ctypes.cast(ctypes.byref(a), ctypes.c_void_p)
+        check_run(
+            lib().rs_launch(self.handle, g, b, c, int(smem), _stream_ptr(stream), ptrs),
+            f"launch of {self.name}",
+        )
+
+
+def _dim3(d):
+    if isinstance(d, int):
+        return (d, 1, 1)
+    d = tuple(int(x) for x in d)
+    return d + (1,) * (3 - len(d))
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    h = getattr(stream, "cuda_stream", None)
+    if h is not None:
+        return ctypes.c_void_p(int(h))
+    return stream
+
+
+_modules: dict = {}
+
+
+def load_module(source: str, name_exprs, opts=(), program_name="rise.cu") -> Module:
+    key = (source, tuple(name_exprs), tuple(opts))
+    mod = _modules.get(key)
+    if mod is None:
+        cubin, lowered = compile_cubin(source, name_exprs, opts, program_name)
+        mod = Module(cubin, lowered)
+        _modules[key] = mod
+    return mod
+
+
+# memory helpers ------------------------------------------------------------
+
+
+class DeviceBuffer:
+    """A raw device allocation owned by the runtime (rs_malloc/rs_free)."""
+
+    def __init__(self, nbytes: int):
+        init()
+        self.nbytes = int(nbytes)
+        self.ptr = ctypes.c_void_p()
+        check_run(lib().rs_malloc(ctypes.byref(self.ptr), self.nbytes), "rs_malloc")
+
+    def __del__(self):
+        try:
+            if self.ptr and _lib is not None:
+                _lib.rs_free(self.ptr)
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def memcpy_htod(dst, src_host_ptr, nbytes, stream=None):
+    check_run(lib().rs_memcpy_htod(_vp(dst), _vp(src_host_ptr), nbytes, _stream_ptr(stream)), "htod")
+
+
+def memcpy_dtoh(dst_host_ptr, src, nbytes, stream=None):
+    check_run(lib().rs_memcpy_dtoh(_vp(dst_host_ptr), _vp(src), nbytes, _stream_ptr(stream)), "dtoh")
+
+
+def memset_d8(dst, value, nbytes, stream=None):
+    check_run(lib().rs_memset_d8(_vp(dst), value, nbytes, _stream_ptr(stream)), "memset")
+
+
+def stream_synchronize(stream=None):
+    check_run(lib().rs_stream_synchronize(_stream_ptr(stream)), "stream sync")
+
+
+def _vp(p):
+    if isinstance(p, ctypes.c_void_p):
+        return p
+    if isinstance(p, DeviceBuffer):
+        return p.ptr
+    return ctypes.c_void_p(int(p))
+
+
+class Event:
+    def __init__(self):
+        init()
+        self.h = ctypes.c_void_p()
+        check_run(lib().rs_event_create(ctypes.byref(self.h)), "event create")
+
+    def record(self, stream=None):
+        check_run(lib().rs_event_record(self.h, _stream_ptr(stream)), "event record")
+
+    def synchronize(self):
+        check_run(lib().rs_event_synchronize(self.h), "event sync")
+
+    def elapsed_ms(self, end: "Event") -> float:
+        v = ctypes.c_float()
+        check_run(lib().rs_event_elapsed_ms(ctypes.byref(v), self.h, end.h), "elapsed")
+        return float(v.value)
+
+
+def tma_desc_2d_f32(base_ptr, dim0, dim1, row_stride_bytes, box0, box1, swizzle=0):
+    """Encode a CUtensorMap (128 bytes, returned as a ctypes array that can be
+    passed by value as a __grid_constant__ kernel argument)."""
+    desc = TensorMap()
+    check_run(
+        lib().rs_tma_desc_2d_f32(ctypes.byref(desc), _vp(base_ptr), dim0, dim1, row_stride_bytes,
+                                 box0, box1, swizzle),
+        "rs_tma_desc_2d_f32",
+    )
+    return desc
+
+
+class TensorMap(ctypes.Structure):
+    _pack_ = 64
+    _fields_ = [("words", ctypes.c_uint64 * 16)]

@@ -1,0 +1,97 @@
+"""GPU parity of the sm100a back end against the oracle (SURVEY.md §8 c/d).
+
+Bit-exact where the kernel preserves the program's order (generic kernels,
+`rowfold`); fp64 error bound where a template reassociates (`reduce`)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2201_03611_b200 import compile_program, emit_cuda, programs, run_cuda
+
+pytestmark = pytest.mark.gpu
+
+
+def _mv(strategy):
+    return compile_program(programs.MV, strategy, name="mv")
+
+
+@pytest.mark.parametrize("n,m", [(256, 512), (100, 64), (33, 1028), (8192, 8192)])
+def test_mv_global_rowfold_bit_exact(gpu, n, m):
+    c = _mv(programs.MV_GLOBAL_STRATEGY)
+    code = emit_cuda(c.unit)
+    assert code.plan["stages"][0]["kind"] == "rowfold"
+    M = oracle.rng_inputs(2, n, m)
+    x = oracle.rng_inputs(3, m)
+    out = run_cuda(code, c.unit, {"n": n, "m": m}, [M, x], as_numpy=True)
+    np.testing.assert_array_equal(out, oracle.mv(M, x))
+
+
+@pytest.mark.parametrize("n,m,s", [(256, 512, 32), (64, 36, 8), (96, 130, 32)])
+def test_mv_opt_rowfold_bit_exact(gpu, n, m, s):
+    c = _mv(programs.MV_OPT_STRATEGY)
+    code = emit_cuda(c.unit)
+    M = oracle.rng_inputs(4, n, m)
+    x = oracle.rng_inputs(5, m)
+    out = run_cuda(code, c.unit, {"n": n, "m": m, "s": s}, [M, x], as_numpy=True)
+    np.testing.assert_array_equal(out, oracle.mv(M, x))
+
+
+@pytest.mark.parametrize("key", ["gemv", "gemv_opt"])
+def test_mv_generic_kernel_bit_exact(gpu, key):
+    cfg = programs.CONFIGS[key]
+    c = compile_program(cfg["source"], cfg["strategy"], name="mv")
+    code = emit_cuda(c.unit, idioms=False)
+    nats = {"n": 96, "m": 80, "s": 16}
+    M = oracle.rng_inputs(6, 96, 80)
+    x = oracle.rng_inputs(7, 80)
+    out = run_cuda(code, c.unit, nats, [M, x], as_numpy=True)
+    np.testing.assert_array_equal(out, oracle.mv(M, x))
+
+
+def test_mv_known_answer(gpu):
+    # test_interpreter.py:37-40: M = [[1,2,3],[4,5,6]], x = [1,1,1] -> [6, 15]
+    c = _mv(programs.MV_GLOBAL_STRATEGY)
+    code = emit_cuda(c.unit)
+    out = run_cuda(code, c.unit, {"n": 2, "m": 3}, [[[1, 2, 3], [4, 5, 6]], [1, 1, 1]])
+    assert out == [np.float32(6), np.float32(15)]
+
+
+@pytest.mark.parametrize("n", [1 << 20, 1 << 24, 4096 + 4])
+def test_dot_reduce_within_bound(gpu, n):
+    c = compile_program(programs.DOT, programs.DOT_STRATEGY, name="dot")
+    code = emit_cuda(c.unit)
+    assert code.plan["stages"][0]["kind"] == "reduce"
+    a = oracle.rng_inputs(1, n)
+    b = oracle.rng_inputs(11, n)
+    got = run_cuda(code, c.unit, {"n": n}, [a, b], as_numpy=True)[0]
+    v64, abs_sum = oracle.dot_f64(a, b)
+    per_thread = -(-n // (1184 * 256))
+    assert abs(float(got) - v64) <= oracle.reassociated_dot_bound(n, abs_sum, 4 * per_thread)
+
+
+def test_dot_deterministic(gpu):
+    c = compile_program(programs.DOT, programs.DOT_STRATEGY, name="dot")
+    code = emit_cuda(c.unit)
+    a = oracle.rng_inputs(1, 1 << 22)
+    b = oracle.rng_inputs(2, 1 << 22)
+    r = [run_cuda(code, c.unit, {"n": 1 << 22}, [a, b], as_numpy=True)[0] for _ in range(3)]
+    assert r[0] == r[1] == r[2]
+
+
+def test_dot_generic_serial_bit_exact(gpu):
+    c = compile_program(programs.DOT, programs.DOT_STRATEGY, name="dot")
+    code = emit_cuda(c.unit, idioms=False)
+    a = oracle.rng_inputs(1, 4096)
+    b = oracle.rng_inputs(2, 4096)
+    got = run_cuda(code, c.unit, {"n": 4096}, [a, b], as_numpy=True)[0]
+    assert got == oracle.dot(a, b)
+
+
+def test_conv_generic_bit_exact(gpu):
+    c = compile_program(programs.CONV, None, name="conv")
+    code = emit_cuda(c.unit)
+    img = oracle.rng_inputs(3, 67, 45)
+    w = (np.array([[1, 2, 1], [2, 4, 2], [1, 2, 1]], np.float32) / 16).astype(np.float32)
+    out = run_cuda(code, c.unit, {"n": 67, "m": 45}, [img, w], as_numpy=True).reshape(67, 45)
+    np.testing.assert_array_equal(out, oracle.conv3x3(img, w))

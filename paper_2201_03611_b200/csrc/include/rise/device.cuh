@@ -77,6 +77,25 @@ RS_DEVICE void rs_bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned 
       : "memory");
 }
 
+// A CUtensorMap passed by value as a __grid_constant__ kernel parameter.
+struct alignas(64) rs_tmap {
+  unsigned long long words[16];
+};
+
+RS_DEVICE void rs_tmap_prefetch(const rs_tmap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(map)) : "memory");
+}
+
+// 2-D TMA tile load (coordinates: inner c0, outer c1) into shared memory,
+// completion counted in bytes on `bar`.
+RS_DEVICE void rs_tma_load_2d(void* dst, const rs_tmap* map, int c0, int c1, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          rs_smem_addr(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(rs_smem_addr(bar))
+      : "memory");
+}
+
 // 128-bit streaming global load that does not allocate in L1.
 RS_DEVICE float4 rs_ldg_stream(const float4* p) {
   float4 r;

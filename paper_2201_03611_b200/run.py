@@ -159,8 +159,10 @@ class Executable:
             return ctypes.c_void_p(temps[extra["name"]].data_ptr())
         if kind == "tma2d":
             base = _dptr(buffers[extra["buf"]]) if extra["buf"] in buffers else temps[extra["buf"]].data_ptr()
+            base += 4 * eval_py(extra.get("offset", "0"), self.nats)
             dims = [eval_py(d, self.nats) for d in extra["dims"]]
-            return rt.tma_desc_2d_f32(base, dims[0], dims[1], dims[0] * 4, extra["box"][0], extra["box"][1],
+            pitch = eval_py(extra.get("pitch", extra["dims"][0]), self.nats)
+            return rt.tma_desc_2d_f32(base, dims[0], dims[1], pitch * 4, extra["box"][0], extra["box"][1],
                                       extra.get("swizzle", 0))
         raise InterpreterError(f"unknown extra kernel argument {kind!r}")
 

@@ -1,0 +1,242 @@
+"""`rowfold` template: a parallel map over rows, each row a sequential fold.
+
+Matches (after the parallel loops are collapsed into a flat row index f):
+
+    for each row f (parallel):            # parForGlobal chain, or
+        acc = INIT                        # parForWorkGroup > parForLocal
+        for j < K:  acc = STEP(acc, A1[base1(f) + j], ..., X1[c + j], ...)
+        POST(acc)                         # e.g. output[f] = acc
+
+where every j-dependent load is unit-stride in j: `row streams` (base
+depends on the row, affine in f: base = c0 + f * pitch) and `shared streams`
+(base independent of the row, e.g. the vector x of gemv).
+
+Order: PRESERVED.  One thread folds one row in j order with the program's own
+STEP expression (rendered with the round-to-nearest intrinsics), so results
+are bit-identical to the reference's sequential semantics.
+
+Data movement (the part the template adds): a ring of RS_STAGES shared-memory
+stages.  Per stage and row stream, the TMA engine loads RS_KT/32 boxes of
+[32 rows x 32 floats] from a 2-D tensor map (rows = f, inner = j) with the
+128-byte swizzle, so lane l reading row l, 16-byte chunk c touches physical
+chunk c ^ (l & 7): conflict-free LDS.128.  Shared streams arrive by 1-D bulk
+copy.  One elected lane arms the stage's mbarrier with the expected bytes and
+issues every copy (a handful of TMA instructions per stage instead of one
+bulk copy per row); the warp consumes stage t while stages t+1.. are in
+flight.  Block = one warp = 32 rows.
+"""
+
+from __future__ import annotations
+
+from . import lir
+from ._ref import nat
+from .emit_cuda import NatRenderer, ValueRenderer, kernel_head, py_expr
+
+ROWS = 32
+KT = 128  # columns per stage (4 TMA boxes of 32 columns)
+STAGES = 6
+BOX_BYTES = 32 * 32 * 4
+
+
+def affine_in_flat_row(base, loops, assumptions):
+    """(c0, pitch, preconditions) with base == c0 + f * pitch for the flat row
+    index f of the collapsed loops, or None."""
+    row_vars = [v for v, _ in loops]
+    zero = {v: nat.Const(0) for v in row_vars}
+    c0 = nat.normalize(nat.substitute(base, zero), assumptions)
+    coeffs = []
+    for v in row_vars:
+        one = dict(zero)
+        one[v] = nat.Const(1)
+        two = dict(zero)
+        two[v] = nat.Const(2)
+        c1 = nat.normalize(nat.substitute(base, one) - c0, assumptions)
+        c2 = nat.normalize(nat.substitute(base, two) - c0, assumptions)
+        if not nat.equal(c2, nat.normalize(c1 * nat.Const(2)), assumptions):
+            return None
+        if any(x in nat.free_vars(c1) for x in row_vars):
+            return None
+        coeffs.append(c1)
+    pitch = coeffs[-1]
+    pre = []
+    inner = nat.Const(1)
+    for k in range(len(loops) - 1, -1, -1):
+        want = nat.normalize(pitch * inner, assumptions)
+        if not nat.equal(coeffs[k], want, assumptions):
+            pre.append(f"({py_expr(coeffs[k])}) == ({py_expr(want)})")
+        inner = inner * loops[k][1]
+    return c0, pitch, pre
+
+
+def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_coef):
+    """Render the kernel; returns (text, plan) or None if a precondition
+    cannot be expressed."""
+    acc, init, loop, post = shape
+    step = loop.body.value
+    r = NatRenderer(prog.clamps)
+    nrows = nat.Const(1)
+    for _, b in loops:
+        nrows = nrows * b
+    nrows = nat.normalize(nrows, prog.assumptions)
+
+    rs_list = list(dict.fromkeys(row_streams.values()))
+    sh_list = list(dict.fromkeys(shared_streams.values()))
+    pre = [f"({py_expr(loop.bound)}) % 4 == 0"]
+    tmaps = []
+    for k, (buf, base) in enumerate(rs_list):
+        aff = affine_in_flat_row(base, loops, prog.assumptions)
+        if aff is None:
+            return None
+        c0, pitch, apre = aff
+        pre += apre + [f"({py_expr(c0)}) % 4 == 0", f"({py_expr(pitch)}) % 4 == 0", f"({py_expr(pitch)}) > 0"]
+        tmaps.append({"kind": "tma2d", "buf": buf, "offset": py_expr(c0), "dims": [py_expr(loop.bound), py_expr(nrows)],
+                      "pitch": py_expr(pitch), "box": [32, ROWS], "swizzle": 3})
+    for buf, base in sh_list:
+        pre.append(f"({py_expr(base)}) % 4 == 0")
+    pre = list(dict.fromkeys(pre))
+
+    nbox = KT // 32
+    stage_floats = len(rs_list) * nbox * 32 * ROWS + len(sh_list) * KT
+    stage_floats = -(-stage_floats // 256) * 256  # stages stay 1024-byte aligned (128B swizzle)
+    extra = [f"const __grid_constant__ rs_tmap rs_map{k}" for k in range(len(rs_list))]
+    lines = kernel_head(prog, name, temps, launch_bounds=ROWS, extra_params=extra)
+    lines += [
+        f"  constexpr int RS_ROWS = {ROWS}, RS_KT = {KT}, RS_STAGES = {STAGES}, RS_NBOX = {nbox};",
+        f"  constexpr int RS_NROWS = {r(nrows)};",
+        f"  constexpr int RS_K = {r(loop.bound)};",
+        "  constexpr int RS_NT = (RS_K + RS_KT - 1) / RS_KT;",
+        f"  constexpr int RS_STAGE_FLOATS = {stage_floats};",
+        "  extern __shared__ __align__(1024) unsigned char rs_smem_raw[];",
+        "  float* rs_smem = reinterpret_cast<float*>(rs_smem_raw + ((1024u - (rs_smem_addr(rs_smem_raw) & 1023u)) & 1023u));",
+        "  unsigned long long* rs_bar = reinterpret_cast<unsigned long long*>(rs_smem + RS_STAGES * RS_STAGE_FLOATS);",
+        "  const int rs_lane = threadIdx.x;",
+        "  const int rs_row0 = blockIdx.x * RS_ROWS;",
+        "  const bool rs_active = rs_row0 + rs_lane < RS_NROWS;",
+        "  const int rs_f = rs_active ? rs_row0 + rs_lane : RS_NROWS - 1;",
+    ]
+    rest = "rs_f"
+    for k, (var, _b) in enumerate(loops):
+        if k == len(loops) - 1:
+            lines.append(f"  const int {var} = {rest};")
+        else:
+            inner = nat.Const(1)
+            for _, b in loops[k + 1:]:
+                inner = inner * b
+            size_c = r(nat.normalize(inner), 2)
+            lines.append(f"  const int {var} = {rest} / {size_c};")
+            lines.append(f"  const int rs_q{k} = {rest} % {size_c};")
+            rest = f"rs_q{k}"
+    for k, (buf, base) in enumerate(sh_list):
+        lines.append(f"  const float* rs_gx{k} = {buf} + ({r(base)});")
+    # per-lane swizzled chunk offsets (bytes) inside a 128-byte box row
+    lines += [
+        "  const int rs_sw = rs_lane & 7;",
+        "  if (rs_lane == 0) {",
+    ]
+    for k in range(len(rs_list)):
+        lines.append(f"    rs_tmap_prefetch(&rs_map{k});")
+    lines += [
+        "    for (int rs_s = 0; rs_s < RS_STAGES; ++rs_s) rs_mbar_init(&rs_bar[rs_s], 1);",
+        "    rs_fence_barrier_init();",
+        "  }",
+        "  __syncwarp();",
+        "  auto rs_issue = [&](int rs_t) {",
+        "    const int rs_slot = rs_t % RS_STAGES;",
+        "    const int rs_j0 = rs_t * RS_KT;",
+        "    const int rs_kt = RS_K - rs_j0 < RS_KT ? RS_K - rs_j0 : RS_KT;",
+        "    const int rs_nb = (rs_kt + 31) / 32;",
+        "    float* rs_st = rs_smem + rs_slot * RS_STAGE_FLOATS;",
+        "    rs_fence_proxy_async();",
+        "    if (rs_lane == 0) {",
+        f"      rs_mbar_arrive_expect_tx(&rs_bar[rs_slot], (unsigned)(rs_nb * {BOX_BYTES} * {len(rs_list)}"
+        f" + rs_kt * 4 * {len(sh_list)}));",
+    ]
+    for k in range(len(rs_list)):
+        lines += [
+            "      for (int rs_b = 0; rs_b < rs_nb; ++rs_b)",
+            f"        rs_tma_load_2d(rs_st + ({k} * RS_NBOX + rs_b) * 32 * RS_ROWS, &rs_map{k}, rs_j0 + 32 * rs_b, rs_row0,"
+            " &rs_bar[rs_slot]);",
+        ]
+    for k in range(len(sh_list)):
+        off = f"{len(rs_list)} * RS_NBOX * 32 * RS_ROWS + {k} * RS_KT"
+        lines.append(f"      rs_bulk_g2s(rs_st + {off}, rs_gx{k} + rs_j0, (unsigned)rs_kt * 4u, &rs_bar[rs_slot]);")
+    lines += [
+        "    }",
+        "  };",
+        "  for (int rs_t = 0; rs_t < RS_STAGES - 1 && rs_t < RS_NT; ++rs_t) rs_issue(rs_t);",
+    ]
+    vr = ValueRenderer(prog, exact)
+    lines.append(f"  {acc.ctype} {acc.name};")
+    lines.append(f"  {acc.name} = {vr(init.value)};")
+
+    def step_with(comp):
+        def hook(ld):
+            if ld in row_streams:
+                return f"rs_a{rs_list.index(row_streams[ld])}.{comp}"
+            if ld in shared_streams:
+                return f"rs_x{sh_list.index(shared_streams[ld])}.{comp}"
+            return None
+
+        return ValueRenderer(prog, exact, load_hook=hook)(step)
+
+    def chunk(ind):
+        p = " " * ind
+        out = [
+            f"{p}const int rs_box = rs_jj >> 5;",
+            f"{p}const int rs_chunk = ((rs_jj >> 2) & 7) ^ rs_sw;",
+        ]
+        for k in range(len(rs_list)):
+            out.append(
+                f"{p}const float4 rs_a{k} = *reinterpret_cast<const float4*>(rs_st + ({k} * RS_NBOX + rs_box) * 32 * RS_ROWS"
+                f" + rs_lane * 32 + rs_chunk * 4);")
+        for k in range(len(sh_list)):
+            off = f"{len(rs_list)} * RS_NBOX * 32 * RS_ROWS + {k} * RS_KT"
+            out.append(f"{p}const float4 rs_x{k} = *reinterpret_cast<const float4*>(rs_st + {off} + rs_jj);")
+        for comp in ("x", "y", "z", "w"):
+            out.append(f"{p}{acc.name} = {step_with(comp)};")
+        return out
+
+    lines += [
+        "  for (int rs_t = 0; rs_t < RS_NT; ++rs_t) {",
+        "    if (rs_t + RS_STAGES - 1 < RS_NT) rs_issue(rs_t + RS_STAGES - 1);",
+        "    const int rs_slot = rs_t % RS_STAGES;",
+        "    const float* rs_st = rs_smem + rs_slot * RS_STAGE_FLOATS;",
+        "    rs_mbar_wait(&rs_bar[rs_slot], (unsigned)((rs_t / RS_STAGES) & 1));",
+        "    const int rs_kt = RS_K - rs_t * RS_KT < RS_KT ? RS_K - rs_t * RS_KT : RS_KT;",
+        "    if (rs_kt == RS_KT) {",
+        "#pragma unroll",
+        "      for (int rs_jj = 0; rs_jj < RS_KT; rs_jj += 4) {",
+    ]
+    lines += chunk(8)
+    lines += [
+        "      }",
+        "    } else {",
+        "      for (int rs_jj = 0; rs_jj < rs_kt; rs_jj += 4) {",
+    ]
+    lines += chunk(8)
+    lines += [
+        "      }",
+        "    }",
+        "    __syncwarp();",
+        "  }",
+        "  if (rs_active) {",
+    ]
+    from .emit_cuda import GenericKernel, Stage
+
+    for s in post:
+        g = GenericKernel(prog, Stage("serial", s), "_", [], exact)
+        lines += [("    " + x) for x in g.thread(s, 0)]
+    lines += ["  }", "}"]
+    smem = STAGES * stage_floats * 4 + STAGES * 8 + 1024
+    plan = {
+        "name": name,
+        "kind": "rowfold",
+        "rows": py_expr(nrows),
+        "row_block": ROWS,
+        "smem": smem,
+        "pre": pre,
+        "fmad": False,
+        "order": "preserved",
+        "extra_args": tmaps,
+    }
+    return "\n".join(lines) + "\n", plan

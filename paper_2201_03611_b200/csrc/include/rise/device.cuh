@@ -20,7 +20,11 @@ RS_DEVICE float rs_rsqrt_exact(float x) { return __fdiv_rn(1.0f, __fsqrt_rn(x));
 
 // Fast path (MUFU.RSQ); used only where the program is compared under a
 // tolerance (DESIGN.md parity rules).
-RS_DEVICE float rs_rsqrt_fast(float x) { return rsqrtf(x); }
+RS_DEVICE float rs_rsqrt_fast(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 RS_DEVICE unsigned rs_smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));

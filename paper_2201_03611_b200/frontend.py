@@ -50,6 +50,12 @@ def rewrite(typed, strategy_text: str):
 def compile_program(source: str, strategy_text: str | None = None, name: str | None = None,
                     target: str = "opencl", assumptions=()) -> Compiled:
     """RISE text (+ optional .elv strategy) -> ImperativeUnit."""
+    import sys
+
+    # the reference's recursive passes (inference, translation, phrase
+    # substitution) nest deeply on larger programs such as nbody
+    if sys.getrecursionlimit() < 20000:
+        sys.setrecursionlimit(20000)
     pname, typed, free = typed_program(source, assumptions)
     lowered = typed
     asms = list(assumptions)

@@ -23,7 +23,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
-from . import lir, tmpl_rowfold
+from . import lir, tmpl_allpairs, tmpl_rowfold, tmpl_stencil
 from ._ref import nat
 from .emit_cuda import NatRenderer, ValueRenderer, collapse_global_chain, kernel_head, py_expr
 
@@ -37,11 +37,27 @@ class IdiomKernel:
 
 
 def match(prog, stage, base_name, temps, exact):
-    for matcher in (_match_rowfold, _match_reduce):
+    for matcher in (_match_rowfold, _match_reduce, _match_stencil, _match_allpairs):
         out = matcher(prog, stage, base_name, temps, exact)
         if out is not None:
             return out
     return None
+
+
+def _match_allpairs(prog, stage, base_name, temps, exact):
+    out = tmpl_allpairs.match(prog, stage, base_name, temps, exact, parallel_rows)
+    if out is None:
+        return None
+    text, plan = out
+    return IdiomKernel(plan["name"], text, plan)
+
+
+def _match_stencil(prog, stage, base_name, temps, exact):
+    out = tmpl_stencil.match(prog, stage, base_name, temps, exact, parallel_rows)
+    if out is None:
+        return None
+    text, plan = out
+    return IdiomKernel(plan["name"], text, plan)
 
 
 # ---------------------------------------------------------------------------
@@ -161,9 +177,9 @@ def _launch_rowfold(st, nats, sm):
 # ---------------------------------------------------------------------------
 # reduce (reassociated, deterministic)
 
-REDUCE_GRID = 1184  # 8 x 148, fixed: the reduction order never depends on the GPU
+REDUCE_GRID = 592  # 4 x 148 (one wave at <= 64 registers), fixed: the order never depends on the GPU
 REDUCE_BLOCK = 256
-REDUCE_BATCH = 8  # float4 chunks per input loaded before folding (memory-level parallelism)
+REDUCE_BATCH = 4  # float4 chunks per input loaded before folding (memory-level parallelism)
 
 
 def _match_reduce(prog, stage, base_name, temps, exact):
@@ -334,4 +350,6 @@ def _launch_reduce(st, nats, sm):
 LAUNCHERS = {
     "rowfold": _launch_rowfold,
     "reduce": _launch_reduce,
+    "stencil2d": tmpl_stencil.launch,
+    "allpairs": tmpl_allpairs.launch,
 }

@@ -50,6 +50,7 @@ class Load:
     buf: str
     index: object  # nat.Nat (flat)
     ctype: str
+    indices: tuple = ()  # per-dimension indices before flattening (analysis only)
 
 
 @dataclass(frozen=True)
@@ -362,7 +363,8 @@ class Builder:
                 if projs:
                     raise EmitError("tuple projection reached array memory; zips must stay views")
                 buf = self.buffers[b.buf]
-                return Load(buf.name, self.flat(buf, list(pending)), buf.ctype)
+                idx = tuple(self.norm(i) for i in pending) if not buf.deref else ()
+                return Load(buf.name, self.flat(buf, list(pending)), buf.ctype, idx)
             raise EmitError(f"cannot read {p!r}")
         if isinstance(p, dpia.PhraseLiteral):
             return Lit(p.text, _lit_ctype(p))

@@ -1,0 +1,242 @@
+"""`allpairs` template: every target folds over every source (nbody).
+
+Matches a grid stage over targets g < NT whose body is
+
+    [for c < C:]                       # a small, constant component loop
+      acc = INIT(g, c)
+      for j < NS:  S(g, c, j, acc)      # any private computation ending in
+                                        #   acc = f(acc, ...)
+      POST(g, c, acc)                   # e.g. output[3g + c] = vel + dt * acc
+
+where every load that depends on j reads a "source stream" B[a*j + off]
+with a constant stride a and 0 <= off < a (off from c and constant inner
+loops), and every other load is j-invariant (the target's own data).
+
+Order: each (g, c) fold still runs over j = 0, 1, ..., NS-1 in order.  The
+template fuses the c loop into the j loop (independent accumulators, so
+each fold's sequence of operations is unchanged), tiles j through shared
+memory (all threads of a block read the same source element: broadcast
+LDS), and register-blocks RB targets per thread so one staged source serves
+RB x C accumulators; the compiler CSEs the per-pair work shared by the C
+components (distance, rsqrt).  This template is emitted with fast math
+(FMA contraction, MUFU rsqrt): parity is the tolerance of DESIGN.md (no
+worse than the reference's own fp32 left fold, measured against fp64).
+"""
+
+from __future__ import annotations
+
+from . import lir
+from ._ref import nat
+from .emit_cuda import GenericKernel, NatRenderer, Stage, ValueRenderer, kernel_head, py_expr
+
+BLOCK = 128
+RB = 4  # targets per thread
+JT = 256  # sources per shared-memory tile
+
+
+def _split(body):
+    """-> (cvar, C, acc, init, jloop, post) or None"""
+    cvar, C = None, nat.Const(1)
+    if isinstance(body, lir.For):
+        cvar, C = body.var, body.bound
+        body = body.body
+        if not isinstance(C, nat.Const) or C.value > 8:
+            return None
+    if not (isinstance(body, lir.Alloc) and body.dims == () and body.space == "Private"):
+        return None
+    acc = lir.ScalarRef(body.name, body.ctype)
+    stmts = body.body.stmts if isinstance(body.body, lir.Seq) else [body.body]
+    if len(stmts) < 2:
+        return None
+    init, jloop, post = stmts[0], stmts[1], stmts[2:]
+    if not (isinstance(init, lir.Assign) and init.target == acc and isinstance(jloop, lir.For)):
+        return None
+    for s in post:
+        for t in lir.walk(s):
+            if isinstance(t, (lir.For, lir.ParFor, lir.Alloc, lir.DoubleBuffer)):
+                return None
+    # the fold body may only write acc and its own private temporaries
+    local = {s.name for s in lir.walk(jloop.body) if isinstance(s, lir.Alloc)}
+    for s in lir.walk(jloop.body):
+        if isinstance(s, (lir.ParFor, lir.DoubleBuffer, lir.Raw)):
+            return None
+        if isinstance(s, lir.Alloc) and s.space == "Global":
+            return None
+        if isinstance(s, lir.Assign):
+            t = s.target
+            if isinstance(t, lir.ScalarRef) and t != acc and t.name not in local:
+                return None
+            if isinstance(t, lir.Store) and t.buf not in local:
+                return None
+    return cvar, C, acc, init, jloop, post
+
+
+def _const_loop_bounds(stmt):
+    out = {}
+    for s in lir.walk(stmt):
+        if isinstance(s, lir.For):
+            out[s.var] = s.bound
+    return out
+
+
+def _source_stride(index, j, allowed_off_vars, bounds, cvar, C):
+    """index = a*j + off with 0 <= off < a: returns a (int) or None."""
+    zero = nat.normalize(nat.substitute(index, {j: nat.Const(0)}))
+    one = nat.normalize(nat.substitute(index, {j: nat.Const(1)}))
+    two = nat.normalize(nat.substitute(index, {j: nat.Const(2)}))
+    a = nat.normalize(one - zero)
+    if not isinstance(a, nat.Const) or a.value < 1:
+        return None
+    if not nat.equal(nat.normalize(two - zero), nat.Const(2 * a.value)):
+        return None
+    off_vars = nat.free_vars(zero)
+    if not off_vars <= allowed_off_vars:
+        return None
+    # range of off over the constant loops
+    lo = hi = nat.normalize(nat.substitute(zero, {v: nat.Const(0) for v in off_vars}))
+    if not isinstance(lo, nat.Const):
+        return None
+    lo = hi = lo.value
+    for v in off_vars:
+        b = C if v == cvar else bounds.get(v)
+        if not isinstance(b, nat.Const):
+            return None
+        z = {u: nat.Const(0) for u in off_vars}
+        o = dict(z)
+        o[v] = nat.Const(1)
+        coef = nat.normalize(nat.substitute(zero, o) - nat.substitute(zero, z))
+        if not isinstance(coef, nat.Const):
+            return None
+        span = coef.value * (b.value - 1)
+        lo += min(0, span)
+        hi += max(0, span)
+    if lo < 0 or hi >= a.value:
+        return None
+    return a.value
+
+
+def match(prog, stage, base_name, temps, exact, parallel_rows):
+    loops, body = parallel_rows(stage)
+    if loops is None or len(loops) != 1 or stage.kind != "grid":
+        return None
+    (gv, NT), = loops
+    sp = _split(body)
+    if sp is None:
+        return None
+    cvar, C, acc, init, jloop, post = sp
+    j = jloop.var
+    NS = jloop.bound
+    if not nat.free_vars(NS) <= set(prog.nat_params):
+        return None
+    bounds = _const_loop_bounds(jloop.body)
+    allowed_off = set(bounds) | ({cvar} if cvar else set())
+    streams = {}  # buf -> stride
+    for _t, value in lir.stmt_exprs(jloop.body):
+        for ld in lir.expr_loads(value):
+            if j not in nat.free_vars(ld.index):
+                continue
+            buf = prog.buffers[ld.buf]
+            if buf.role != "input":
+                return None
+            a = _source_stride(ld.index, j, allowed_off, bounds, cvar, C)
+            if a is None or streams.get(ld.buf, a) != a:
+                return None
+            streams[ld.buf] = a
+    if not streams:
+        return None
+    s_list = sorted(streams.items())
+    name = f"{base_name}_allpairs"
+    r = NatRenderer(prog.clamps)
+    fast = False  # fast math: FMA contraction + MUFU rsqrt
+
+    def hook(ld):
+        if ld.buf in streams and j in nat.free_vars(ld.index):
+            k = [b for b, _ in s_list].index(ld.buf)
+            a = streams[ld.buf]
+            return f"rs_s{k}[({r(ld.index)}) - {a} * rs_j0]"
+        return None
+
+    g = GenericKernel(prog, Stage("serial", jloop.body), "_", [], exact=fast)
+    g.r = ValueRenderer(prog, exact=fast, load_hook=hook)
+    step_lines = g.thread(jloop.body, 2)
+    gp = GenericKernel(prog, Stage("serial", lir.Seq(list(post))), "_", [], exact=fast)
+    post_lines = gp.thread(lir.Seq(list(post)), 3)
+    vinit = ValueRenderer(prog, exact=fast)(init.value)
+    Cv = C.value
+    cdecl = f"const int {cvar}" if cvar else "const int rs_c_unused"
+    lines = kernel_head(prog, name, temps, launch_bounds=BLOCK)
+    lines += [
+        f"  constexpr int RS_NT = {r(NT)}, RS_NS = {r(NS)}, RS_JT = {JT}, RS_RB = {RB}, RS_C = {Cv};",
+    ]
+    for k, (buf, a) in enumerate(s_list):
+        lines.append(f"  __shared__ float rs_s{k}[RS_JT * {a}];")
+    lines += [
+        f"  const int rs_g0 = blockIdx.x * ({BLOCK} * RS_RB) + threadIdx.x;",
+        "  int rs_j0 = 0;",
+        f"  auto rs_step = [&](const int {gv}, {cdecl}, const int {j}, {acc.ctype} {acc.name}) -> {acc.ctype} {{",
+    ]
+    lines += step_lines
+    lines += [
+        f"    return {acc.name};",
+        "  };",
+        f"  {acc.ctype} rs_acc[RS_RB][RS_C];",
+        "#pragma unroll",
+        "  for (int rs_r = 0; rs_r < RS_RB; ++rs_r) {",
+        f"    const int {gv} = min(rs_g0 + rs_r * {BLOCK}, RS_NT - 1);",
+        "#pragma unroll",
+        "    for (int rs_c = 0; rs_c < RS_C; ++rs_c) {",
+        f"      {cdecl} = rs_c;",
+        f"      rs_acc[rs_r][rs_c] = {vinit};",
+        "    }",
+        "  }",
+        "  for (rs_j0 = 0; rs_j0 < RS_NS; rs_j0 += RS_JT) {",
+        "    const int rs_jn = RS_NS - rs_j0 < RS_JT ? RS_NS - rs_j0 : RS_JT;",
+        "    __syncthreads();",
+    ]
+    for k, (buf, a) in enumerate(s_list):
+        lines += [
+            f"    for (int rs_e = threadIdx.x; rs_e < rs_jn * {a}; rs_e += {BLOCK})",
+            f"      rs_s{k}[rs_e] = {buf}[{a} * rs_j0 + rs_e];",
+        ]
+    lines += [
+        "    __syncthreads();",
+        "#pragma unroll 2",
+        "    for (int rs_jj = 0; rs_jj < rs_jn; ++rs_jj) {",
+        "#pragma unroll",
+        "      for (int rs_r = 0; rs_r < RS_RB; ++rs_r) {",
+        f"        const int rs_g = min(rs_g0 + rs_r * {BLOCK}, RS_NT - 1);",
+        "#pragma unroll",
+        "        for (int rs_c = 0; rs_c < RS_C; ++rs_c)",
+        "          rs_acc[rs_r][rs_c] = rs_step(rs_g, rs_c, rs_j0 + rs_jj, rs_acc[rs_r][rs_c]);",
+        "      }",
+        "    }",
+        "  }",
+        "#pragma unroll",
+        "  for (int rs_r = 0; rs_r < RS_RB; ++rs_r) {",
+        f"    const int {gv} = rs_g0 + rs_r * {BLOCK};",
+        f"    if ({gv} < RS_NT) {{",
+        "#pragma unroll",
+        "      for (int rs_c = 0; rs_c < RS_C; ++rs_c) {",
+        f"        {cdecl} = rs_c;",
+        f"        {acc.ctype} {acc.name} = rs_acc[rs_r][rs_c];",
+    ]
+    lines += post_lines
+    lines += ["      }", "    }", "  }", "}"]
+    plan = {
+        "name": name,
+        "kind": "allpairs",
+        "targets": py_expr(NT),
+        "per_block": BLOCK * RB,
+        "block": BLOCK,
+        "fmad": True,
+        "order": "preserved-fold, fast-math",
+        "pre": [],
+    }
+    return "\n".join(lines) + "\n", plan
+
+
+def launch(st, nats, sm):
+    from .emit_cuda import eval_py
+
+    nt = eval_py(st["targets"], nats)
+    return (max(1, -(-nt // st["per_block"])), 1, 1), (st["block"], 1, 1), 0, (1, 1, 1)

@@ -66,7 +66,8 @@ def test_dot_reduce_within_bound(gpu, n):
     b = oracle.rng_inputs(11, n)
     got = run_cuda(code, c.unit, {"n": n}, [a, b], as_numpy=True)[0]
     v64, abs_sum = oracle.dot_f64(a, b)
-    per_thread = -(-n // (1184 * 256))
+    from paper_2201_03611_b200 import idioms
+    per_thread = -(-n // (idioms.REDUCE_GRID * idioms.REDUCE_BLOCK))
     assert abs(float(got) - v64) <= oracle.reassociated_dot_bound(n, abs_sum, 4 * per_thread)
 
 
@@ -95,3 +96,56 @@ def test_conv_generic_bit_exact(gpu):
     w = (np.array([[1, 2, 1], [2, 4, 2], [1, 2, 1]], np.float32) / 16).astype(np.float32)
     out = run_cuda(code, c.unit, {"n": 67, "m": 45}, [img, w], as_numpy=True).reshape(67, 45)
     np.testing.assert_array_equal(out, oracle.conv3x3(img, w))
+
+
+W3 = (np.array([[1, 2, 1], [2, 4, 2], [1, 2, 1]], np.float32) / 16).astype(np.float32)
+
+
+@pytest.mark.parametrize("n,m", [(67, 45), (64, 32), (130, 97), (8192, 8192)])
+def test_conv_stencil_bit_exact(gpu, n, m):
+    c = compile_program(programs.CONV, None, name="conv")
+    code = emit_cuda(c.unit)
+    assert code.plan["stages"][0]["kind"] == "stencil2d"
+    img = oracle.rng_inputs(3, n, m)
+    out = run_cuda(code, c.unit, {"n": n, "m": m}, [img, W3], as_numpy=True).reshape(n, m)
+    np.testing.assert_array_equal(out, oracle.conv3x3(img, W3))
+
+
+def _nbody_inputs(n, seed=5):
+    rng = np.random.default_rng(seed)
+    pos = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    vel = rng.uniform(-0.1, 0.1, (n, 3)).astype(np.float32)
+    mass = rng.uniform(0.5, 1.5, n).astype(np.float32)
+    return pos, vel, mass
+
+
+def _nbody_abs_terms(pos, mass, first, count):
+    p = pos.astype(np.float64)
+    out = np.zeros((count, 3))
+    for k, i in enumerate(range(first, first + count)):
+        d = p - p[i]
+        r2 = (d * d).sum(1) + 0.01
+        s = mass / (r2 * np.sqrt(r2))
+        out[k] = (np.abs(d) * s[:, None]).sum(0)
+    return out
+
+
+@pytest.mark.parametrize("n,first,count", [(4096, 0, 4096), (131072, 1000, 192), (1000, 0, 1000)])
+def test_nbody_allpairs_within_tolerance(gpu, n, first, count):
+    c = compile_program(programs.NBODY, None, name="nbody")
+    code = emit_cuda(c.unit)
+    assert code.plan["stages"][0]["kind"] == "allpairs"
+    pos, vel, mass = _nbody_inputs(n)
+    got = run_cuda(code, c.unit, {"n": n}, [pos, vel, mass], as_numpy=True).reshape(n, 3)[first:first + count]
+    ref32 = oracle.nbody(pos, vel, mass, first, count)
+    ref64 = vel[first:first + count].astype(np.float64) + 0.01 * oracle.nbody_acc_f64(pos, mass, first, count)
+    bound = 2 * np.abs(ref32 - ref64) + 16 * oracle.U * 0.01 * _nbody_abs_terms(pos, mass, first, count)
+    assert np.all(np.abs(got - ref64) <= bound + 1e-12), float(np.max(np.abs(got - ref64) - bound))
+
+
+def test_nbody_generic_exact_bit_exact(gpu):
+    c = compile_program(programs.NBODY, None, name="nbody")
+    code = emit_cuda(c.unit, idioms=False)
+    pos, vel, mass = _nbody_inputs(300)
+    got = run_cuda(code, c.unit, {"n": 300}, [pos, vel, mass], as_numpy=True).reshape(300, 3)
+    np.testing.assert_array_equal(got, oracle.nbody(pos, vel, mass))

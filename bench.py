@@ -337,7 +337,7 @@ def run_ours(args, rank, world, local_rank):
         # write a buffer larger than L2, then read another one so the dirty
         # lines are written back here and not inside the next timed step
         flush.zero_()
-        torch.sum(sweep, out=sink)
+        torch.sum(sweep, dim=0, out=sink)
 
     def step():
         exe(*dev_in, out=out, stream=stream)

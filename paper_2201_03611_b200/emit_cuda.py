@@ -312,7 +312,10 @@ class GenericKernel:
             return [decl] + self.thread(s.body, ind)
         if isinstance(s, (lir.For, lir.ParFor)):
             head = f"{p}for (int {s.var} = 0; {s.var} < {self.nat(s.bound)}; {s.var} += 1) {{"
-            return [head] + self.thread(s.body, ind + 1) + [f"{p}}}"]
+            pre = []
+            if isinstance(s.bound, nat.Const) and s.bound.value <= 16:
+                pre = ["#pragma unroll"]  # small windows: constant register indices
+            return pre + [head] + self.thread(s.body, ind + 1) + [f"{p}}}"]
         if isinstance(s, lir.IfLess):
             return (
                 [f"{p}if ({self.nat(s.lhs)} < {self.nat(s.threshold)}) {{"]

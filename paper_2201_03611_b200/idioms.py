@@ -177,9 +177,13 @@ def _launch_rowfold(st, nats, sm):
 # ---------------------------------------------------------------------------
 # reduce (reassociated, deterministic)
 
-REDUCE_GRID = 592  # 4 x 148 (one wave at <= 64 registers), fixed: the order never depends on the GPU
-REDUCE_BLOCK = 256
-REDUCE_BATCH = 4  # float4 chunks per input loaded before folding (memory-level parallelism)
+import os  # noqa: E402
+
+# Fixed launch shape: the reduction order depends only on these constants and
+# the problem size, never on the GPU.  (Overridable for tuning sweeps only.)
+REDUCE_GRID = int(os.environ.get("RISE_REDUCE_GRID", "1184"))
+REDUCE_BLOCK = int(os.environ.get("RISE_REDUCE_BLOCK", "256"))
+REDUCE_BATCH = int(os.environ.get("RISE_REDUCE_BATCH", "4"))  # float4 chunks per input in flight per thread
 
 
 def _match_reduce(prog, stage, base_name, temps, exact):

@@ -29,9 +29,13 @@ from . import lir
 from ._ref import nat
 from .emit_cuda import GenericKernel, NatRenderer, Stage, ValueRenderer, kernel_head, py_expr
 
-BLOCK = 128
-RB = 4  # targets per thread
-JT = 256  # sources per shared-memory tile
+import os
+
+# 64-thread blocks x 2 targets per thread: 1024 blocks for 131072 bodies, so
+# the per-SM load is balanced to ~1% and each SM holds ~14 warps
+BLOCK = int(os.environ.get("RISE_ALLPAIRS_BLOCK", "64"))
+RB = int(os.environ.get("RISE_ALLPAIRS_RB", "2"))  # targets per thread
+JT = int(os.environ.get("RISE_ALLPAIRS_JT", "512"))  # sources per shared-memory tile
 
 
 def _split(body):

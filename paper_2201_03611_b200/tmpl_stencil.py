@@ -2,21 +2,27 @@
 through clamped neighbourhood indices (padClamp2D + slide2D programs).
 
 Matches a stage whose parallel loops collapse to exactly two variables
-(r < R, c < C) and in which every load of some 2-D array A has per-dimension
+(r < R, c < C) and in which every load of some 2-D input A has per-dimension
 indices  clamp(r + o0, H-1)  and  clamp(c + o1, W-1),  where o0 / o1 are
 affine in sequential loop variables with constant bounds (the window
 offsets).  The offsets' ranges [omin, omax] give the halo.
 
 Order: PRESERVED.  The body is the generic emitter's code for the program's
 own loop nest (row sums, then the fold of the row sums, with the
-round-to-nearest intrinsics); only the loads of A are redirected to a
-shared-memory tile.  Bit-identical to the reference's semantics.
+round-to-nearest intrinsics); only the loads of A are redirected.
+Bit-identical to the reference's semantics.
 
-Data movement: one block computes a TR x TC output tile (32 x 8 threads,
-RPT consecutive rows per thread so window rows are reused from registers);
-the (TR + halo) x (TC + halo) input footprint is staged once into shared
-memory, with the clamp applied while staging (padClamp semantics, so border
-tiles need no special case).  Stores are 128-byte coalesced rows.
+Data movement:
+* a block computes a TR x TC = 64 x 128 output tile (32 x 8 threads, each
+  thread RPT = 8 rows x CPT = 4 adjacent columns);
+* the tile's input footprint (rows + halo, columns + halo, left edge padded
+  to a 16-byte boundary) is staged into shared memory by ONE 2-D TMA load
+  for interior tiles; border tiles stage through clamped loads (padClamp
+  semantics), so no per-access clamp remains in the compute;
+* each thread copies its (RPT + halo) x (CPT + halo) window from shared
+  memory into registers (LDS.128 for the aligned middle columns), and the
+  body's loads of A become constant-indexed register reads after unrolling
+  — one staged value serves every output of the window that uses it.
 """
 
 from __future__ import annotations
@@ -25,10 +31,10 @@ from . import lir
 from ._ref import nat
 from .emit_cuda import GenericKernel, NatRenderer, Stage, ValueRenderer, kernel_head, py_expr
 
-TC = 32  # columns per tile = blockDim.x
-TY = 8  # blockDim.y
-RPT = 8  # consecutive output rows per thread
-TR = TY * RPT
+TX, TY = 32, 8
+RPT = 8  # output rows per thread
+CPT = 4  # adjacent output columns per thread
+TR, TC = TY * RPT, TX * CPT
 
 
 def _seq_loop_bounds(stmt):
@@ -47,7 +53,8 @@ def _offset_range(expr, base_var, loop_bounds):
     off = nat.normalize(expr - nat.Var(base_var))
     if base_var in nat.free_vars(off):
         return None
-    lo = hi = nat.normalize(nat.substitute(off, {v: nat.Const(0) for v in nat.free_vars(off)}))
+    zero = {v: nat.Const(0) for v in nat.free_vars(off)}
+    lo = nat.normalize(nat.substitute(off, zero))
     if not isinstance(lo, nat.Const):
         return None
     lo = hi = lo.value
@@ -55,12 +62,11 @@ def _offset_range(expr, base_var, loop_bounds):
         b = loop_bounds.get(v)
         if b is None or not isinstance(b, nat.Const) or b.value < 1:
             return None
-        zero = {u: nat.Const(0) for u in nat.free_vars(off)}
         one = dict(zero)
         one[v] = nat.Const(1)
-        coef = nat.normalize(nat.substitute(off, one) - nat.substitute(off, zero))
         two = dict(zero)
         two[v] = nat.Const(2)
+        coef = nat.normalize(nat.substitute(off, one) - nat.substitute(off, zero))
         coef2 = nat.normalize(nat.substitute(off, two) - nat.substitute(off, zero))
         if not (isinstance(coef, nat.Const) and isinstance(coef2, nat.Const) and coef2.value == 2 * coef.value):
             return None
@@ -76,13 +82,12 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         return None
     (rv, R), (cv, C) = loops
     bounds = _seq_loop_bounds(body)
-    tiled = {}  # buf -> [omin0, omax0, omin1, omax1, H-1, W-1]
+    tiled = {}  # buf -> [omin0, omax0, omin1, omax1]
     for _t, value in lir.stmt_exprs(body):
         for ld in lir.expr_loads(value):
             if not any(v in prog.clamps for v in nat.free_vars(ld.index)):
-                if rv in nat.free_vars(ld.index) or cv in nat.free_vars(ld.index):
-                    if ld.buf in tiled:
-                        return None
+                if ld.buf in tiled:
+                    return None
                 continue
             buf = prog.buffers[ld.buf]
             if buf.role != "input" or len(buf.dims) != 2 or len(ld.indices) != 2:
@@ -105,67 +110,131 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     if len(tiled) != 1:
         return None
     (abuf, (o0lo, o0hi, o1lo, o1hi)), = tiled.items()
-    if o0hi - o0lo > 16 or o1hi - o1lo > 16:
+    if not (o0lo <= 0 <= o0hi and o1lo <= 0 <= o1hi) or o0hi - o0lo > 8 or o1hi - o1lo > 8:
         return None
     A = prog.buffers[abuf]
     name = f"{base_name}_stencil"
     r = NatRenderer(prog.clamps)
-    HR = TR + (o0hi - o0lo)
-    HC = TC + (o1hi - o1lo)
+    hr = o0hi - o0lo  # halo rows
+    hcl, hcr = -o1lo, o1hi  # halo columns left / right
+    lp = -(-hcl // 4) * 4  # left pad, keeps the thread's columns 16-byte aligned
+    sw = -(-(lp + TC + hcr) // 4) * 4  # staged row width (multiple of 16 bytes)
+    sr = TR + hr  # staged rows
+    wr, wc = RPT + hr, CPT + hcl + hcr  # register window
+
+    # small row/column-invariant inputs (e.g. the 3x3 weights) live in registers
+    small = {}
+    for _t, value in lir.stmt_exprs(body):
+        for ld in lir.expr_loads(value):
+            b = prog.buffers[ld.buf]
+            if ld.buf == abuf or b.role != "input" or rv in nat.free_vars(ld.index) or cv in nat.free_vars(ld.index):
+                continue
+            size = nat.Const(1)
+            for d in b.dims:
+                size = size * d
+            size = nat.normalize(size)
+            if isinstance(size, nat.Const) and size.value <= 64:
+                small[ld.buf] = size.value
 
     def hook(ld):
+        if ld.buf in small:
+            return f"rs_p_{ld.buf}[{r(ld.index)}]"
         if ld.buf != abuf:
             return None
         e0, e1 = ld.indices
-        in0 = prog.clamps[e0.name][0]
-        in1 = prog.clamps[e1.name][0]
-        return f"rs_tile[(({r(in0)}) - rs_tr0) * {HC} + (({r(in1)}) - rs_tc0)]"
+        off0 = nat.normalize(prog.clamps[e0.name][0] - nat.Var(rv))
+        off1 = nat.normalize(prog.clamps[e1.name][0] - nat.Var(cv))
+        return f"rs_v[rs_k + ({r(off0)}) + {-o0lo}][rs_q + ({r(off1)}) + {hcl}]"
 
     g = GenericKernel(prog, Stage("serial", body), "_", [], exact)
     g.r = ValueRenderer(prog, exact, load_hook=hook)
-    body_lines = g.thread(body, 3)
-
-    lines = kernel_head(prog, name, temps, launch_bounds=TC * TY)
+    body_lines = g.thread(body, 4)
+    hdim = r(nat.normalize(A.dims[0] - nat.Const(1)))
+    wdim = r(nat.normalize(A.dims[1] - nat.Const(1)))
+    lines = kernel_head(prog, name, temps, launch_bounds=TX * TY,
+                        extra_params=["const __grid_constant__ rs_tmap rs_map"])
     lines += [
         f"  constexpr int RS_R = {r(R)}, RS_C = {r(C)};",
-        f"  __shared__ float rs_tile[{HR} * {HC}];",
+        f"  constexpr int RS_H = {r(A.dims[0])}, RS_W = {r(A.dims[1])};",
+        f"  constexpr int RS_SR = {sr}, RS_SW = {sw};",
+        "  __shared__ __align__(128) float rs_tile[RS_SR * RS_SW];",
+        "  __shared__ __align__(8) unsigned long long rs_bar;",
         f"  const int rs_r0 = blockIdx.y * {TR}, rs_c0 = blockIdx.x * {TC};",
-        f"  const int rs_tr0 = rs_r0 + ({o0lo}), rs_tc0 = rs_c0 + ({o1lo});",
-        f"  for (int rs_e = threadIdx.y * {TC} + threadIdx.x; rs_e < {HR * HC}; rs_e += {TC * TY}) {{",
-        f"    const int rs_y = rs_e / {HC}, rs_x = rs_e % {HC};",
-        f"    rs_tile[rs_e] = {abuf}[rs_clamp(rs_tr0 + rs_y, {r(nat.normalize(A.dims[0] - nat.Const(1)))}) * "
-        f"({r(A.dims[1])}) + rs_clamp(rs_tc0 + rs_x, {r(nat.normalize(A.dims[1] - nat.Const(1)))})];",
-        "  }",
-        "  __syncthreads();",
-        f"  const int {cv} = rs_c0 + threadIdx.x;",
-        f"  if (rs_r0 + {TR} <= RS_R && rs_c0 + {TC} <= RS_C) {{",
-        "    // interior tile: unguarded, so window loads are shared across the unrolled rows",
-        "#pragma unroll",
-        f"    for (int rs_k = 0; rs_k < {RPT}; ++rs_k) {{",
-        f"      const int {rv} = rs_r0 + threadIdx.y * {RPT} + rs_k;",
-        "      {",
-    ]
-    lines += ["    " + x for x in body_lines]
-    lines += [
-        "      }",
+        f"  const int rs_tr0 = rs_r0 + ({o0lo}), rs_tc0 = rs_c0 - {lp};",
+        "  const int rs_tid = threadIdx.y * blockDim.x + threadIdx.x;",
+        "  const bool rs_interior = rs_tr0 >= 0 && rs_tr0 + RS_SR <= RS_H && rs_tc0 >= 0 && rs_tc0 + RS_SW <= RS_W;",
+        "  if (rs_interior) {",
+        "    if (rs_tid == 0) {",
+        "      rs_mbar_init(&rs_bar, 1);",
+        "      rs_fence_barrier_init();",
+        "      rs_mbar_arrive_expect_tx(&rs_bar, (unsigned)(RS_SR * RS_SW * 4));",
+        "      rs_tma_load_2d(rs_tile, &rs_map, rs_tc0, rs_tr0, &rs_bar);",
         "    }",
+        "    __syncthreads();",
+        "    rs_mbar_wait(&rs_bar, 0u);",
         "  } else {",
-        f"    for (int rs_k = 0; rs_k < {RPT}; ++rs_k) {{",
-        f"      const int {rv} = rs_r0 + threadIdx.y * {RPT} + rs_k;",
-        f"      if ({rv} < RS_R && {cv} < RS_C) {{",
+        f"    for (int rs_e = rs_tid; rs_e < RS_SR * RS_SW; rs_e += {TX * TY}) {{",
+        "      const int rs_y = rs_e / RS_SW, rs_x = rs_e - (rs_e / RS_SW) * RS_SW;",
+        f"      rs_tile[rs_e] = {abuf}[rs_clamp(rs_tr0 + rs_y, {hdim}) * RS_W + rs_clamp(rs_tc0 + rs_x, {wdim})];",
+        "    }",
+        "    __syncthreads();",
+        "  }",
     ]
-    lines += ["    " + x for x in body_lines]
-    lines += ["      }", "    }", "  }", "}"]
+    for buf, size in sorted(small.items()):
+        lines += [
+            f"  float rs_p_{buf}[{size}];",
+            "#pragma unroll",
+            f"  for (int rs_e = 0; rs_e < {size}; ++rs_e) rs_p_{buf}[rs_e] = __ldg({buf} + rs_e);",
+        ]
+    lines += [
+        "  // this thread's register window (tile rows ty*RPT.., columns lp + tx*CPT - hcl..)",
+        f"  float rs_v[{wr}][{wc}];",
+        "#pragma unroll",
+        f"  for (int rs_y = 0; rs_y < {wr}; ++rs_y) {{",
+        f"    const float* rs_row = rs_tile + (threadIdx.y * {RPT} + rs_y) * RS_SW + {lp} + threadIdx.x * {CPT};",
+        "    const float4 rs_mid = *reinterpret_cast<const float4*>(rs_row);",
+    ]
+    for k in range(hcl):
+        lines.append(f"    rs_v[rs_y][{k}] = rs_row[{k - hcl}];")
+    lines += [
+        f"    rs_v[rs_y][{hcl}] = rs_mid.x; rs_v[rs_y][{hcl + 1}] = rs_mid.y;",
+        f"    rs_v[rs_y][{hcl + 2}] = rs_mid.z; rs_v[rs_y][{hcl + 3}] = rs_mid.w;",
+    ]
+    for k in range(hcr):
+        lines.append(f"    rs_v[rs_y][{hcl + CPT + k}] = rs_row[{CPT + k}];")
+    lines += [
+        "  }",
+    ]
+    for guarded in (False, True):
+        if not guarded:
+            lines.append(f"  if (rs_r0 + {TR} <= RS_R && rs_c0 + {TC} <= RS_C) {{")
+        else:
+            lines.append("  } else {")
+        lines += [
+            "#pragma unroll",
+            f"  for (int rs_k = 0; rs_k < {RPT}; ++rs_k) {{",
+            "#pragma unroll",
+            f"    for (int rs_q = 0; rs_q < {CPT}; ++rs_q) {{",
+            f"      const int {rv} = rs_r0 + threadIdx.y * {RPT} + rs_k;",
+            f"      const int {cv} = rs_c0 + threadIdx.x * {CPT} + rs_q;",
+            f"      if ({'true' if not guarded else f'{rv} < RS_R && {cv} < RS_C'}) {{",
+        ]
+        lines += body_lines
+        lines += ["      }", "    }", "  }"]
+    lines += ["  }", "}"]
     plan = {
         "name": name,
         "kind": "stencil2d",
         "rows": py_expr(R),
         "cols": py_expr(C),
         "tile": [TR, TC],
-        "block": [TC, TY],
+        "block": [TX, TY],
         "fmad": False,
         "order": "preserved",
-        "pre": [],
+        "pre": [f"({py_expr(A.dims[1])}) % 4 == 0"],
+        "extra_args": [{"kind": "tma2d", "buf": abuf, "offset": "0",
+                        "dims": [py_expr(A.dims[1]), py_expr(A.dims[0])], "pitch": py_expr(A.dims[1]),
+                        "box": [sw, sr], "swizzle": 0}],
     }
     return "\n".join(lines) + "\n", plan
 

@@ -1,0 +1,116 @@
+"""The sm100a emit target on CPU: deterministic text, template selection,
+NVRTC compilation for sm_100a (no GPU needed), and the drop-in behaviour of
+`emit` next to the reference's targets."""
+
+import re
+
+import pytest
+
+from paper_2201_03611_b200 import compile_program, emit, emit_cuda, lir, programs, runtime
+from paper_2201_03611_b200._ref import codegen, errors, nat
+
+EXPECTED_TEMPLATE = {
+    "dot": "reduce",
+    "gemv": "rowfold",
+    "gemv_opt": "rowfold",
+    "conv": "stencil2d",
+    "nbody": "allpairs",
+}
+
+
+def _code(key):
+    return emit_cuda(programs.compile_config(key).unit)
+
+
+@pytest.mark.parametrize("key", sorted(programs.CONFIGS))
+def test_emission_is_byte_stable(key):
+    assert _code(key).text == _code(key).text
+
+
+@pytest.mark.parametrize("key,kind", sorted(EXPECTED_TEMPLATE.items()))
+def test_benchmark_programs_select_their_template(key, kind):
+    code = _code(key)
+    assert [s["kind"] for s in code.plan["stages"]] == [kind]
+    # the generic kernel stays in the text as the fallback
+    assert "fallback" in code.plan["stages"][0]
+
+
+@pytest.mark.parametrize("key", sorted(programs.CONFIGS))
+def test_templates_compile_for_sm100a_with_nvrtc(key):
+    code = _code(key)
+    nats = programs.CONFIGS[key]["nats"]
+    targs = ", ".join(str(nats[p]) for p in code.plan["nat_params"])
+    names = []
+    for st in code.plan["stages"]:
+        for s in (st, st.get("fallback")):
+            if s:
+                names.append(f"{s['name']}<{targs}>")
+    cubin, lowered = runtime.compile_cubin(code.text, names, ["--fmad=false"])
+    assert cubin[:4] == b"\x7fELF" and len(lowered) == len(names)
+
+
+def test_emit_keeps_reference_targets_and_rejects_cuda():
+    c = programs.compile_config("gemv")
+    assert emit(c.unit, "openmp") == codegen.emit(c.unit, "openmp")
+    with pytest.raises(errors.EmitError):
+        emit(c.unit, "cuda")  # test_codegen.py:151-154 must keep holding
+    assert emit(c.unit, "sm100a").startswith("// rise-b200 sm100a")
+
+
+def test_mv_opt_indices_match_listing_10():
+    # tests/golden/mv_opt_kernel.cl:8-10: M[i + lId*m + m*s*wgId], x[i], output[lId + s*wgId]
+    c = programs.compile_config("gemv_opt")
+    prog = lir.build(c.unit)
+    loads = [ld for _t, v in lir.stmt_exprs(prog.body) for ld in lir.expr_loads(v)]
+    M = next(ld for ld in loads if ld.buf == "M")
+    x = next(ld for ld in loads if ld.buf == "x")
+    V = nat.Var
+    assert nat.equal(M.index, V("i") + V("lId") * V("m") + V("m") * V("s") * V("wgId"))
+    assert nat.equal(x.index, V("i"))
+    stores = [t for t, _v in lir.stmt_exprs(prog.body) if isinstance(t, lir.Store)]
+    assert nat.equal(stores[0].index, V("lId") + V("s") * V("wgId"))
+
+
+def test_generic_kernel_maps_nested_mapglobal_to_one_grid_loop():
+    # SURVEY §8 a (i): nested mapGlobal must not share one id
+    src = "fun(M: Array[4, Array[3, f32]] => M |> mapGlobal(fun(r => r |> mapGlobal(fun(v => v * 2.0f)))))"
+    code = emit_cuda(compile_program(src, name="nested").unit)
+    assert "rs_f < rs_total" in code.text and "rs_total = 12" in code.text
+
+
+def test_local_memory_becomes_shared_with_barriers():
+    # SURVEY §8 a (ii): toMem(Local) between mapLocal stages needs a barrier
+    src = ("depFun((n: Nat, m: Nat) => fun(M: Array[n, Array[m, f32]] => M |> mapWorkGroup(fun(row => "
+           "row |> mapLocal(fun(z => z * 2.0f)) |> toMem(Local) |> mapLocal(fun(z => z + 1.0f))))))")
+    code = emit_cuda(compile_program(src, name="stages").unit)
+    assert "__shared__ float tmp[m];" in code.text
+    body = code.text[code.text.index("stagesKernel("):]
+    assert body.count("__syncthreads();") >= 2
+
+
+def test_global_temporary_splits_kernels():
+    # SURVEY §8 a (iii): toMem(Global) between parallel stages -> two kernels
+    src = ("depFun((n: Nat) => fun(xs: Array[n, f32] => xs |> mapGlobal(fun(v => v * 2.0f)) "
+           "|> toMem(Global) |> mapGlobal(fun(v => v + 1.0f))))")
+    code = emit_cuda(compile_program(src, name="twoStage").unit)
+    assert [s["name"] for s in code.plan["stages"]] == ["twoStageKernel_s0", "twoStageKernel_s1"]
+    assert code.plan["temps"] and code.plan["temps"][0]["size"] == "n"
+
+
+def test_plan_round_trips_through_the_text():
+    from paper_2201_03611_b200 import plan_of
+
+    code = _code("gemv")
+    assert plan_of(code.text) == code.plan
+
+
+def test_exact_mode_uses_round_to_nearest_intrinsics():
+    code = _code("gemv")
+    kernel = code.text[code.text.index("mvKernel_rowfold("):]
+    assert "__fadd_rn(" in kernel and "__fmul_rn(" in kernel
+    assert not re.search(r"accum = \(accum \+", kernel)
+
+
+def test_sizes_are_template_parameters():
+    code = _code("gemv")
+    assert "template <int n, int m>" in code.text

@@ -1,0 +1,225 @@
+// rise/gemm_tc.cuh — fp32 GEMM on the 5th-generation tensor cores (tcgen05)
+// with the 3xTF32 split, for the `gemm_tc` template (tmpl_gemm.py).
+//
+//   C[M x N] = A[M x K] * Bt[N x K]^T      (both operands K-major)
+//
+// 3xTF32: x = hi + lo with hi = x with the low 13 mantissa bits cleared
+// (exactly representable in TF32) and lo = x - hi (exact in fp32).  Then
+//   A*B ~= A_hi*B_hi + A_hi*B_lo + A_lo*B_hi
+// (the dropped A_lo*B_lo and the TF32 rounding of lo are ~2^-22 relative),
+// accumulated in fp32 in tensor memory: fp32-level accuracy at TF32 speed.
+//
+// CTA tile 128 x 128, K step 32 (one 128-byte swizzle atom), 3-stage ring:
+//   warp 0      TMA producer: raw fp32 A / B tiles -> shared memory (SW128)
+//   warp 1      TMEM allocator + MMA issuer (one elected thread): 12
+//               tcgen05.mma.kind::tf32 (M=128, N=128, K=8) per stage into a
+//               128-column fp32 TMEM accumulator; tcgen05.commit frees stages
+//   warps 2..5  split each landed stage in place (raw -> hi, new lo tiles),
+//               then the epilogue: tcgen05.ld 32x32b -> registers -> global
+#pragma once
+#include "device.cuh"
+
+namespace rise_gemm {
+
+constexpr int BM = 128, BN = 128, BK = 32;
+constexpr int STAGES = 3;
+constexpr int TILE_A = BM * BK * 4;  // 16 KiB
+constexpr int TILE_B = BN * BK * 4;  // 16 KiB
+constexpr int STAGE_BYTES = 2 * (TILE_A + TILE_B);
+constexpr int THREADS = 192;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr unsigned TMEM_COLS = BN;
+
+// instruction descriptor, kind::tf32: D f32 (bits 4-5 = 1), A/B tf32 (bits
+// 7-9, 10-12 = 2), both K-major (bits 15, 16 = 0), N >> 3 at bit 17, M >> 4
+// at bit 24
+constexpr unsigned IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(BM >> 4) << 24);
+
+// shared-memory matrix descriptor, K-major, 128-byte swizzle: start >> 4,
+// LBO = 1 (unused for swizzled K-major), SBO = 1024 B (8 rows x 128 B) >> 4,
+// version 1 (sm_100), layout type 2 (SWIZZLE_128B)
+RS_DEVICE unsigned long long smem_desc(unsigned saddr) {
+  unsigned long long d = (unsigned long long)((saddr >> 4) & 0x3FFFu);
+  d |= 1ull << 16;
+  d |= (unsigned long long)(1024 >> 4) << 32;
+  d |= 1ull << 46;
+  d |= 2ull << 61;
+  return d;
+}
+
+RS_DEVICE void mma(unsigned tmem_d, unsigned long long adesc, unsigned long long bdesc, unsigned accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+
+RS_DEVICE void commit(unsigned long long* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   rs_smem_addr(bar))
+               : "memory");
+}
+
+RS_DEVICE void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+RS_DEVICE void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+RS_DEVICE void tmem_alloc(unsigned* slot) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(rs_smem_addr(slot)),
+               "r"(TMEM_COLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+RS_DEVICE void tmem_dealloc(unsigned taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(TMEM_COLS) : "memory");
+}
+
+// 32 consecutive fp32 columns of this warp's 32 TMEM lanes -> 32 registers
+RS_DEVICE void tmem_ld32(unsigned taddr, unsigned* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+RS_DEVICE float4 split_hi(float4 v) {
+  return make_float4(__uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u),
+                     __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u),
+                     __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u),
+                     __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u));
+}
+
+// C (row pitch ldc) for the 128 x 128 tile at (blockIdx.y, blockIdx.x)
+template <int K>
+RS_DEVICE void gemm_3xtf32(float* __restrict__ C, int ldc, const rs_tmap* mapA, const rs_tmap* mapB) {
+  extern __shared__ __align__(1024) unsigned char rs_gemm_smem_raw[];
+  unsigned char* smem =
+      rs_gemm_smem_raw + ((1024u - (rs_smem_addr(rs_gemm_smem_raw) & 1023u)) & 1023u);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + STAGES * STAGE_BYTES);
+  unsigned long long* full = bars;
+  unsigned long long* conv = bars + STAGES;
+  unsigned long long* empty = bars + 2 * STAGES;
+  unsigned long long* tmem_full = bars + 3 * STAGES;
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 3 * STAGES + 1);
+
+  constexpr int KB = K / BK;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  auto a_raw = [&](int s) { return smem + s * STAGE_BYTES; };
+  auto a_lo = [&](int s) { return smem + s * STAGE_BYTES + TILE_A; };
+  auto b_raw = [&](int s) { return smem + s * STAGE_BYTES + 2 * TILE_A; };
+  auto b_lo = [&](int s) { return smem + s * STAGE_BYTES + 2 * TILE_A + TILE_B; };
+
+  if (threadIdx.x == 0) {
+    rs_tmap_prefetch(mapA);
+    rs_tmap_prefetch(mapB);
+    for (int s = 0; s < STAGES; ++s) {
+      rs_mbar_init(&full[s], 1);
+      rs_mbar_init(&conv[s], 4);
+      rs_mbar_init(&empty[s], 1);
+    }
+    rs_mbar_init(tmem_full, 1);
+    rs_fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const unsigned tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % STAGES;
+        const unsigned ph = (unsigned)((kb / STAGES) & 1);
+        rs_mbar_wait(&empty[s], ph ^ 1u);
+        rs_mbar_arrive_expect_tx(&full[s], TILE_A + TILE_B);
+        rs_tma_load_2d(a_raw(s), mapA, kb * BK, m0, &full[s]);
+        rs_tma_load_2d(b_raw(s), mapB, kb * BK, n0, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % STAGES;
+        const unsigned ph = (unsigned)((kb / STAGES) & 1);
+        rs_mbar_wait(&full[s], ph);
+        rs_mbar_wait(&conv[s], ph);
+        fence_after();
+        const unsigned long long ahi = smem_desc(rs_smem_addr(a_raw(s)));
+        const unsigned long long alo = smem_desc(rs_smem_addr(a_lo(s)));
+        const unsigned long long bhi = smem_desc(rs_smem_addr(b_raw(s)));
+        const unsigned long long blo = smem_desc(rs_smem_addr(b_lo(s)));
+#pragma unroll
+        for (int k = 0; k < BK / 8; ++k) {
+          const unsigned long long off = (unsigned long long)(k * 32) >> 4;  // 8 tf32 = 32 bytes
+          mma(tmem, alo + off, bhi + off, (kb | k) != 0);
+          mma(tmem, ahi + off, blo + off, 1u);
+          mma(tmem, ahi + off, bhi + off, 1u);
+        }
+        commit(&empty[s]);
+      }
+      commit(tmem_full);
+    }
+    __syncwarp();
+  } else {
+    // split stages in place: raw -> hi (low 13 mantissa bits cleared), lo = raw - hi
+    const int t = threadIdx.x - 64;
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % STAGES;
+      const unsigned ph = (unsigned)((kb / STAGES) & 1);
+      rs_mbar_wait(&full[s], ph);
+      float4* ar = reinterpret_cast<float4*>(a_raw(s));
+      float4* al = reinterpret_cast<float4*>(a_lo(s));
+      float4* br = reinterpret_cast<float4*>(b_raw(s));
+      float4* bl = reinterpret_cast<float4*>(b_lo(s));
+#pragma unroll 4
+      for (int i = t; i < TILE_A / 16; i += 128) {
+        const float4 v = ar[i];
+        const float4 h = split_hi(v);
+        ar[i] = h;
+        al[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+      }
+#pragma unroll 4
+      for (int i = t; i < TILE_B / 16; i += 128) {
+        const float4 v = br[i];
+        const float4 h = split_hi(v);
+        br[i] = h;
+        bl[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+      }
+      rs_fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) rs_mbar_arrive(&conv[s]);
+    }
+    // epilogue: TMEM lanes [32q, 32q+32) belong to warp (q mod 4)
+    rs_mbar_wait(tmem_full, 0u);
+    fence_after();
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    float* crow = C + (long long)(m0 + row) * ldc + n0;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      unsigned r[32];
+      tmem_ld32(tmem + ((unsigned)(q * 32) << 16) + (unsigned)c0, r);
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        *reinterpret_cast<float4*>(crow + c0 + j) =
+            make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                        __uint_as_float(r[j + 3]));
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    tmem_dealloc(tmem);
+  }
+}
+
+}  // namespace rise_gemm

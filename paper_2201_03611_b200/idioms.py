@@ -23,7 +23,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
-from . import lir, tmpl_allpairs, tmpl_rowfold, tmpl_stencil
+from . import lir, tmpl_allpairs, tmpl_gemm, tmpl_rowfold, tmpl_stencil
 from ._ref import nat
 from .emit_cuda import NatRenderer, ValueRenderer, collapse_global_chain, kernel_head, py_expr
 
@@ -37,11 +37,19 @@ class IdiomKernel:
 
 
 def match(prog, stage, base_name, temps, exact):
-    for matcher in (_match_rowfold, _match_reduce, _match_stencil, _match_allpairs):
+    for matcher in (_match_gemm, _match_rowfold, _match_reduce, _match_stencil, _match_allpairs):
         out = matcher(prog, stage, base_name, temps, exact)
         if out is not None:
             return out
     return None
+
+
+def _match_gemm(prog, stage, base_name, temps, exact):
+    out = tmpl_gemm.match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape)
+    if out is None:
+        return None
+    text, plan = out
+    return IdiomKernel(plan["name"], text, plan, includes=["rise/gemm_tc.cuh"])
 
 
 def _match_allpairs(prog, stage, base_name, temps, exact):
@@ -183,7 +191,7 @@ import os  # noqa: E402
 # the problem size, never on the GPU.  (Overridable for tuning sweeps only.)
 REDUCE_GRID = int(os.environ.get("RISE_REDUCE_GRID", "1184"))
 REDUCE_BLOCK = int(os.environ.get("RISE_REDUCE_BLOCK", "256"))
-REDUCE_BATCH = int(os.environ.get("RISE_REDUCE_BATCH", "4"))  # float4 chunks per input in flight per thread
+REDUCE_BATCH = int(os.environ.get("RISE_REDUCE_BATCH", "8"))  # float4 chunks per input in flight per thread
 
 
 def _match_reduce(prog, stage, base_name, temps, exact):
@@ -356,4 +364,5 @@ LAUNCHERS = {
     "reduce": _launch_reduce,
     "stencil2d": tmpl_stencil.launch,
     "allpairs": tmpl_allpairs.launch,
+    "gemm_tc": tmpl_gemm.launch,
 }

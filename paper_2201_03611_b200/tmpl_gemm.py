@@ -1,0 +1,95 @@
+"""`gemm_tc` template: the dense contraction on tcgen05 tensor cores (3xTF32).
+
+Matches the sgemm program's loop nest (programs.SGEMM_BT, SURVEY.md §8 c):
+
+    for i < M, j < N (parallel):
+        acc = 0.0f
+        for p < K:  acc = acc + A[i*K + p] * Bt[j*K + p]     (either product order)
+        output[i*N + j] = acc
+
+and instantiates rise/gemm_tc.cuh: TMA-fed, 128x128 CTA tiles, fp32
+accumulation in tensor memory, operands split hi/lo in shared memory.
+
+Order/precision: REASSOCIATED.  The tensor core sums K in its own order and
+the operands pass through the 3xTF32 split, so parity is the fp64 error
+bound |C - C64| <= 2 K u (|A||B|) of SURVEY.md §8 d, not bit equality.
+"""
+
+from __future__ import annotations
+
+from . import lir
+from ._ref import nat
+from .emit_cuda import NatRenderer, kernel_head, py_expr
+
+
+def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
+    loops, body = parallel_rows(stage)
+    if loops is None or len(loops) != 2 or stage.kind != "grid":
+        return None
+    (iv, M), (jv, N) = loops
+    shape = fold_shape(body)
+    if shape is None:
+        return None
+    acc, init, loop, post = shape
+    if not (isinstance(init.value, lir.Lit) and init.value.text in ("0.0f", "0f", "0.0")):
+        return None
+    p, K = loop.var, loop.bound
+    step = loop.body.value
+    if not (isinstance(step, lir.Bin) and step.op == "+" and step.a == acc and isinstance(step.b, lir.Bin)
+            and step.b.op == "*" and isinstance(step.b.a, lir.Load) and isinstance(step.b.b, lir.Load)
+            and step.ctype == "float"):
+        return None
+    x, y = step.b.a, step.b.b
+    V = nat.Var
+
+    def is_row(ld, var):
+        return nat.equal(ld.index, nat.normalize(V(var) * K + V(p)), prog.assumptions)
+
+    if is_row(x, iv) and is_row(y, jv):
+        a_ld, b_ld = x, y
+    elif is_row(y, iv) and is_row(x, jv):
+        a_ld, b_ld = y, x
+    else:
+        return None
+    for ld in (a_ld, b_ld):
+        if prog.buffers[ld.buf].role != "input":
+            return None
+    if len(post) != 1:
+        return None
+    st = post[0]
+    if not (isinstance(st, lir.Assign) and isinstance(st.target, lir.Store) and st.value == acc
+            and nat.equal(st.target.index, nat.normalize(V(iv) * N + V(jv)), prog.assumptions)):
+        return None
+    name = f"{base_name}_gemm"
+    r = NatRenderer(prog.clamps)
+    extra = ["const __grid_constant__ rs_tmap rs_mapA", "const __grid_constant__ rs_tmap rs_mapB"]
+    lines = kernel_head(prog, name, temps, launch_bounds="192, 1", extra_params=extra)
+    lines += [
+        f"  rise_gemm::gemm_3xtf32<{r(K)}>({st.target.buf}, {r(N)}, &rs_mapA, &rs_mapB);",
+        "}",
+    ]
+    plan = {
+        "name": name,
+        "kind": "gemm_tc",
+        "M": py_expr(M),
+        "N": py_expr(N),
+        "fmad": False,
+        "order": "3xtf32 tensor-core (reassociated)",
+        "pre": [f"({py_expr(M)}) % 128 == 0", f"({py_expr(N)}) % 128 == 0", f"({py_expr(K)}) % 32 == 0"],
+        "smem": 3 * 2 * (16384 + 16384) + 1024 + 256,
+        "extra_args": [
+            {"kind": "tma2d", "buf": a_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(M)], "pitch": py_expr(K),
+             "box": [32, 128], "swizzle": 3},
+            {"kind": "tma2d", "buf": b_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(N)], "pitch": py_expr(K),
+             "box": [32, 128], "swizzle": 3},
+        ],
+    }
+    return "\n".join(lines) + "\n", plan
+
+
+def launch(st, nats, sm):
+    from .emit_cuda import eval_py
+
+    M = eval_py(st["M"], nats)
+    N = eval_py(st["N"], nats)
+    return (N // 128, M // 128, 1), (192, 1, 1), st["smem"], (1, 1, 1)

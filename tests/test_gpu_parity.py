@@ -149,3 +149,37 @@ def test_nbody_generic_exact_bit_exact(gpu):
     pos, vel, mass = _nbody_inputs(300)
     got = run_cuda(code, c.unit, {"n": 300}, [pos, vel, mass], as_numpy=True).reshape(300, 3)
     np.testing.assert_array_equal(got, oracle.nbody(pos, vel, mass))
+
+
+@pytest.mark.parametrize("n,m,k", [(128, 128, 32), (256, 384, 512), (4096, 4096, 4096)])
+def test_sgemm_tcgen05_within_bound(gpu, n, m, k):
+    c = compile_program(programs.SGEMM_BT, None, name="sgemm")
+    code = emit_cuda(c.unit)
+    assert code.plan["stages"][0]["kind"] == "gemm_tc"
+    A = oracle.rng_inputs(4, n, k)
+    Bt = oracle.rng_inputs(14, m, k)
+    got = run_cuda(code, c.unit, {"n": n, "m": m, "k": k}, [A, Bt], as_numpy=True).reshape(n, m)
+    rows = slice(0, min(n, 256))
+    C64, absC = oracle.sgemm_bt_f64(A[rows], Bt)
+    err = np.abs(got[rows] - C64)
+    assert np.all(err <= oracle.gemm_bound(k, absC)), float(np.max(err / (absC * oracle.U * k)))
+    # 3xTF32 must be far more accurate than plain TF32 (~2^-11 relative)
+    assert float(np.max(err / absC)) < 1e-5
+
+
+def test_sgemm_generic_exact_bit_exact(gpu):
+    c = compile_program(programs.SGEMM_BT, None, name="sgemm")
+    code = emit_cuda(c.unit, idioms=False)
+    A = oracle.rng_inputs(4, 40, 24)
+    Bt = oracle.rng_inputs(5, 33, 24)
+    got = run_cuda(code, c.unit, {"n": 40, "m": 33, "k": 24}, [A, Bt], as_numpy=True).reshape(40, 33)
+    np.testing.assert_array_equal(got, oracle.sgemm_bt(A, Bt))
+
+
+def test_sgemm_falls_back_when_tiles_do_not_divide(gpu):
+    c = compile_program(programs.SGEMM_BT, None, name="sgemm")
+    code = emit_cuda(c.unit)
+    A = oracle.rng_inputs(4, 100, 24)
+    Bt = oracle.rng_inputs(5, 36, 24)
+    got = run_cuda(code, c.unit, {"n": 100, "m": 36, "k": 24}, [A, Bt], as_numpy=True).reshape(100, 36)
+    np.testing.assert_array_equal(got, oracle.sgemm_bt(A, Bt))

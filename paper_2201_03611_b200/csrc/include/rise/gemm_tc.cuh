@@ -9,31 +9,38 @@
 // (the dropped A_lo*B_lo and the TF32 rounding of lo are ~2^-22 relative),
 // accumulated in fp32 in tensor memory: fp32-level accuracy at TF32 speed.
 //
-// CTA tile 128 x 128, K step 32 (one 128-byte swizzle atom), 3-stage ring:
+// CTA tile 128 x BN, K step 32 (one 128-byte swizzle atom), STAGES-deep ring:
 //   warp 0      TMA producer: raw fp32 A / B tiles -> shared memory (SW128)
 //   warp 1      TMEM allocator + MMA issuer (one elected thread): 12
-//               tcgen05.mma.kind::tf32 (M=128, N=128, K=8) per stage into a
-//               128-column fp32 TMEM accumulator; tcgen05.commit frees stages
-//   warps 2..5  split each landed stage in place (raw -> hi, new lo tiles),
+//               tcgen05.mma.kind::tf32 (M=128, N=BN, K=8) per stage into a
+//               BN-column fp32 TMEM accumulator; tcgen05.commit frees stages
+//   warps 2..5  split each landed stage (raw -> hi in place unless the
+//               tensor core already ignores the low 13 bits, new lo tiles),
 //               then the epilogue: tcgen05.ld 32x32b -> registers -> global
 #pragma once
 #include "device.cuh"
 
 namespace rise_gemm {
 
-constexpr int BM = 128, BN = 128, BK = 32;
-constexpr int STAGES = 3;
-constexpr int TILE_A = BM * BK * 4;  // 16 KiB
-constexpr int TILE_B = BN * BK * 4;  // 16 KiB
-constexpr int STAGE_BYTES = 2 * (TILE_A + TILE_B);
-constexpr int THREADS = 192;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr unsigned TMEM_COLS = BN;
+constexpr int BM = 128, BK = 32;
 
-// instruction descriptor, kind::tf32: D f32 (bits 4-5 = 1), A/B tf32 (bits
-// 7-9, 10-12 = 2), both K-major (bits 15, 16 = 0), N >> 3 at bit 17, M >> 4
-// at bit 24
-constexpr unsigned IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(BM >> 4) << 24);
+template <int BN_, int STAGES_>
+struct Cfg {
+  static constexpr int BN = BN_;
+  static constexpr int STAGES = STAGES_;
+  static constexpr int TILE_A = BM * BK * 4;  // 16 KiB
+  static constexpr int TILE_B = BN * BK * 4;  // 16 or 32 KiB
+  static constexpr int STAGE_BYTES = 2 * (TILE_A + TILE_B);
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr unsigned TMEM_COLS = BN;
+  // instruction descriptor, kind::tf32: D f32 (bits 4-5 = 1), A/B tf32
+  // (bits 7-9, 10-12 = 2), both K-major (bits 15, 16 = 0), N >> 3 at bit 17,
+  // M >> 4 at bit 24
+  static constexpr unsigned IDESC =
+      (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(BM >> 4) << 24);
+};
+
+constexpr int THREADS = 192;
 
 // shared-memory matrix descriptor, K-major, 128-byte swizzle: start >> 4,
 // LBO = 1 (unused for swizzled K-major), SBO = 1024 B (8 rows x 128 B) >> 4,
@@ -47,6 +54,7 @@ RS_DEVICE unsigned long long smem_desc(unsigned saddr) {
   return d;
 }
 
+template <unsigned IDESC>
 RS_DEVICE void mma(unsigned tmem_d, unsigned long long adesc, unsigned long long bdesc, unsigned accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -63,15 +71,17 @@ RS_DEVICE void commit(unsigned long long* bar) {
 RS_DEVICE void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 RS_DEVICE void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+template <unsigned COLS>
 RS_DEVICE void tmem_alloc(unsigned* slot) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(rs_smem_addr(slot)),
-               "r"(TMEM_COLS)
+               "r"(COLS)
                : "memory");
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
 }
 
+template <unsigned COLS>
 RS_DEVICE void tmem_dealloc(unsigned taddr) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(TMEM_COLS) : "memory");
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(COLS) : "memory");
 }
 
 // 32 consecutive fp32 columns of this warp's 32 TMEM lanes -> 32 registers
@@ -94,13 +104,27 @@ RS_DEVICE float4 split_hi(float4 v) {
                      __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u));
 }
 
-// C (row pitch ldc) for the 128 x 128 tile at (blockIdx.y, blockIdx.x)
-template <int K>
+template <bool WRITE_HI>
+RS_DEVICE void split_tile(unsigned char* raw, unsigned char* lo, int bytes, int t) {
+  float4* r = reinterpret_cast<float4*>(raw);
+  float4* l = reinterpret_cast<float4*>(lo);
+#pragma unroll 4
+  for (int i = t; i < bytes / 16; i += 128) {
+    const float4 v = r[i];
+    const float4 h = split_hi(v);
+    if (WRITE_HI) r[i] = h;
+    l[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+  }
+}
+
+// C (row pitch ldc) for the 128 x BN tile at (blockIdx.y, blockIdx.x)
+template <int K, int BN, int STAGES, bool WRITE_HI>
 RS_DEVICE void gemm_3xtf32(float* __restrict__ C, int ldc, const rs_tmap* mapA, const rs_tmap* mapB) {
+  using G = Cfg<BN, STAGES>;
   extern __shared__ __align__(1024) unsigned char rs_gemm_smem_raw[];
   unsigned char* smem =
       rs_gemm_smem_raw + ((1024u - (rs_smem_addr(rs_gemm_smem_raw) & 1023u)) & 1023u);
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + STAGES * STAGE_BYTES);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + STAGES * G::STAGE_BYTES);
   unsigned long long* full = bars;
   unsigned long long* conv = bars + STAGES;
   unsigned long long* empty = bars + 2 * STAGES;
@@ -110,10 +134,10 @@ RS_DEVICE void gemm_3xtf32(float* __restrict__ C, int ldc, const rs_tmap* mapA, 
   constexpr int KB = K / BK;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  auto a_raw = [&](int s) { return smem + s * STAGE_BYTES; };
-  auto a_lo = [&](int s) { return smem + s * STAGE_BYTES + TILE_A; };
-  auto b_raw = [&](int s) { return smem + s * STAGE_BYTES + 2 * TILE_A; };
-  auto b_lo = [&](int s) { return smem + s * STAGE_BYTES + 2 * TILE_A + TILE_B; };
+  auto a_raw = [&](int s) { return smem + s * G::STAGE_BYTES; };
+  auto a_lo = [&](int s) { return smem + s * G::STAGE_BYTES + G::TILE_A; };
+  auto b_raw = [&](int s) { return smem + s * G::STAGE_BYTES + 2 * G::TILE_A; };
+  auto b_lo = [&](int s) { return smem + s * G::STAGE_BYTES + 2 * G::TILE_A + G::TILE_B; };
 
   if (threadIdx.x == 0) {
     rs_tmap_prefetch(mapA);
@@ -126,7 +150,7 @@ RS_DEVICE void gemm_3xtf32(float* __restrict__ C, int ldc, const rs_tmap* mapA, 
     rs_mbar_init(tmem_full, 1);
     rs_fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot);
+  if (warp == 1) tmem_alloc<G::TMEM_COLS>(tmem_slot);
   fence_before();
   __syncthreads();
   fence_after();
@@ -138,7 +162,7 @@ RS_DEVICE void gemm_3xtf32(float* __restrict__ C, int ldc, const rs_tmap* mapA, 
         const int s = kb % STAGES;
         const unsigned ph = (unsigned)((kb / STAGES) & 1);
         rs_mbar_wait(&empty[s], ph ^ 1u);
-        rs_mbar_arrive_expect_tx(&full[s], TILE_A + TILE_B);
+        rs_mbar_arrive_expect_tx(&full[s], G::TILE_A + G::TILE_B);
         rs_tma_load_2d(a_raw(s), mapA, kb * BK, m0, &full[s]);
         rs_tma_load_2d(b_raw(s), mapB, kb * BK, n0, &full[s]);
       }
@@ -158,9 +182,9 @@ RS_DEVICE void gemm_3xtf32(float* __restrict__ C, int ldc, const rs_tmap* mapA, 
 #pragma unroll
         for (int k = 0; k < BK / 8; ++k) {
           const unsigned long long off = (unsigned long long)(k * 32) >> 4;  // 8 tf32 = 32 bytes
-          mma(tmem, alo + off, bhi + off, (kb | k) != 0);
-          mma(tmem, ahi + off, blo + off, 1u);
-          mma(tmem, ahi + off, bhi + off, 1u);
+          mma<G::IDESC>(tmem, alo + off, bhi + off, (kb | k) != 0);
+          mma<G::IDESC>(tmem, ahi + off, blo + off, 1u);
+          mma<G::IDESC>(tmem, ahi + off, bhi + off, 1u);
         }
         commit(&empty[s]);
       }
@@ -168,30 +192,13 @@ RS_DEVICE void gemm_3xtf32(float* __restrict__ C, int ldc, const rs_tmap* mapA, 
     }
     __syncwarp();
   } else {
-    // split stages in place: raw -> hi (low 13 mantissa bits cleared), lo = raw - hi
     const int t = threadIdx.x - 64;
     for (int kb = 0; kb < KB; ++kb) {
       const int s = kb % STAGES;
       const unsigned ph = (unsigned)((kb / STAGES) & 1);
       rs_mbar_wait(&full[s], ph);
-      float4* ar = reinterpret_cast<float4*>(a_raw(s));
-      float4* al = reinterpret_cast<float4*>(a_lo(s));
-      float4* br = reinterpret_cast<float4*>(b_raw(s));
-      float4* bl = reinterpret_cast<float4*>(b_lo(s));
-#pragma unroll 4
-      for (int i = t; i < TILE_A / 16; i += 128) {
-        const float4 v = ar[i];
-        const float4 h = split_hi(v);
-        ar[i] = h;
-        al[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-      }
-#pragma unroll 4
-      for (int i = t; i < TILE_B / 16; i += 128) {
-        const float4 v = br[i];
-        const float4 h = split_hi(v);
-        br[i] = h;
-        bl[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-      }
+      split_tile<WRITE_HI>(a_raw(s), a_lo(s), G::TILE_A, t);
+      split_tile<WRITE_HI>(b_raw(s), b_lo(s), G::TILE_B, t);
       rs_fence_proxy_async();
       __syncwarp();
       if (lane == 0) rs_mbar_arrive(&conv[s]);
@@ -218,7 +225,7 @@ RS_DEVICE void gemm_3xtf32(float* __restrict__ C, int ldc, const rs_tmap* mapA, 
   __syncthreads();
   if (warp == 1) {
     fence_after();
-    tmem_dealloc(tmem);
+    tmem_dealloc<G::TMEM_COLS>(tmem);
   }
 }
 

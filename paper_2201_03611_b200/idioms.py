@@ -166,6 +166,8 @@ def _match_rowfold(prog, stage, base_name, temps, exact):
             shared_streams[ld] = (ld.buf, base)
     if not row_streams:
         return None
+    if any(prog.buffers[b].ctype != "float" for b, _ in list(row_streams.values()) + list(shared_streams.values())):
+        return None  # the staging moves fp32 words (float4 views)
     name = f"{base_name}_rowfold"
     out = tmpl_rowfold.emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j)
     if out is None:
@@ -223,6 +225,8 @@ def _match_reduce(prog, stage, base_name, temps, exact):
             return None
     if not streams:
         return None
+    if any(prog.buffers[b].ctype != "float" for b, _ in streams.values()):
+        return None  # float4 streaming loads
     for s in post:  # post may only read the accumulator and write memory
         for t in lir.walk(s):
             if isinstance(t, lir.Assign) and isinstance(t.target, lir.ScalarRef) and t.target != acc:

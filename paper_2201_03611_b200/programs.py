@@ -77,6 +77,22 @@ def nbody = depFun((n: Nat) =>
                    |> fun(r2 => rsqrt(r2) * rsqrt(r2) * rsqrt(r2)))) ))(0.0f)) )) )) ))))
 """
 
+# the same step for a block of t target bodies against all n sources (the
+# per-GPU program of the multi-GPU decomposition, shard.sharded_nbody)
+NBODY_SHARD = """\
+def nbodyShard = depFun((t: Nat, n: Nat) =>
+  fun(tpos: Array[t, Array[3, f32]] => fun(tvel: Array[t, Array[3, f32]] =>
+  fun(pos: Array[n, Array[3, f32]] => fun(mass: Array[n, f32] =>
+    zip(tpos)(tvel) |> mapGlobal(fun(pv =>
+      zip(transpose(pos))(zip(fst(pv))(snd(pv))) |> mapSeq(fun(col =>
+        snd(snd(col)) + 0.01f *
+          (zip(fst(col))(zip(pos)(mass)) |> reduceSeq(Private)(fun(acc, q =>
+             acc + (fst(q) - fst(snd(col))) *
+               (snd(snd(q)) *
+                 ((zip(fst(snd(q)))(fst(pv)) |> reduceSeq(Private)(fun(r2, d => r2 + (fst(d) - snd(d)) * (fst(d) - snd(d))))(0.01f))
+                   |> fun(r2 => rsqrt(r2) * rsqrt(r2) * rsqrt(r2)))) ))(0.0f)) )) )) ))))))
+"""
+
 CONFIGS = {
     "dot": dict(source=DOT, strategy=DOT_STRATEGY, name="dot", nats={"n": 1 << 24}),
     "gemv": dict(source=MV, strategy=MV_GLOBAL_STRATEGY, name="mv", nats={"n": 8192, "m": 8192}),

@@ -1,0 +1,101 @@
+"""Multi-GPU decomposition of the benchmark programs (SURVEY.md §8 e).
+
+One process per GPU; `torch.distributed` is the plumbing (NCCL on GPUs,
+gloo in the CPU tests).  Each function takes the per-rank compute as a
+callable, so the same host logic drives the sm100a kernels in bench.py and
+the oracle in tests/test_shard.py.
+
+* gemv / sgemm: contiguous row bands of M (A); x (B) replicated; results
+  stay sharded or are all-gathered in rank order.
+* dot: contiguous chunks; per-rank partial; all-gather; rank-order fold —
+  never an all-reduce, whose summation order is algorithm-dependent.
+* conv (padClamp2D + slide2D): row bands plus one halo row on each side,
+  exchanged with the neighbours (P2P send/recv); at the global edges the
+  halo is the clamped edge row, so running the unchanged program on the
+  (rows + 2)-row local image and keeping the middle rows is exact.
+* nbody: target blocks; positions and masses all-gathered once per step
+  (the programs.NBODY_SHARD program folds a target block over all sources
+  in the same source order as the single-GPU program).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def row_band(total: int, world: int, rank: int):
+    """Balanced contiguous split: (start, count) of rank's rows."""
+    base, extra = divmod(total, world)
+    start = rank * base + min(rank, extra)
+    return start, base + (1 if rank < extra else 0)
+
+
+def rank_order_sum(partials) -> np.float32:
+    """Deterministic fp32 combination of per-rank partials: a left fold in
+    rank order starting from the first partial."""
+    acc = np.float32(partials[0])
+    for p in partials[1:]:
+        acc = np.float32(acc + np.float32(p))
+    return acc
+
+
+def allgather_rank_order(t, group=None):
+    """All-gather a tensor; returns the list indexed by rank."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t.contiguous(), group=group)
+    return out
+
+
+def halo_exchange_rows(band, group=None):
+    """band: local rows [n_local, m].  Returns [n_local + 2, m] with the
+    neighbours' boundary rows (or the clamped own edge row at the global
+    edges) attached above and below."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    top = band[:1].clone()
+    bottom = band[-1:].clone()
+    recv_top = torch.empty_like(top)
+    recv_bottom = torch.empty_like(bottom)
+    ops = []
+    if rank > 0:
+        ops.append(dist.P2POp(dist.isend, band[:1].contiguous(), rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, recv_top, rank - 1, group))
+    if rank < world - 1:
+        ops.append(dist.P2POp(dist.isend, band[-1:].contiguous(), rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, recv_bottom, rank + 1, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    if rank > 0:
+        top = recv_top
+    if rank < world - 1:
+        bottom = recv_bottom
+    return torch.cat([top, band, bottom], dim=0)
+
+
+def sharded_dot(partial_fn, a_chunk, b_chunk, group=None):
+    """partial_fn(a, b) -> 0-d/1-element tensor partial dot on this rank."""
+    p = partial_fn(a_chunk, b_chunk).reshape(1)
+    parts = allgather_rank_order(p, group)
+    return rank_order_sum([float(x.item()) for x in parts])
+
+
+def sharded_conv(conv_fn, band, group=None):
+    """conv_fn(local_image [r, m]) -> [r, m]; returns this rank's output band."""
+    local = halo_exchange_rows(band, group)
+    return conv_fn(local)[1:-1]
+
+
+def sharded_nbody(step_fn, pos_block, vel_block, mass_block, group=None):
+    """step_fn(target_pos, target_vel, all_pos, all_mass) -> new target vel."""
+    import torch
+
+    all_pos = torch.cat(allgather_rank_order(pos_block, group), dim=0)
+    all_mass = torch.cat(allgather_rank_order(mass_block, group), dim=0)
+    return step_fn(pos_block, vel_block, all_pos, all_mass)

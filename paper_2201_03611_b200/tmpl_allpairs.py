@@ -36,6 +36,7 @@ import os
 BLOCK = int(os.environ.get("RISE_ALLPAIRS_BLOCK", "64"))
 RB = int(os.environ.get("RISE_ALLPAIRS_RB", "2"))  # targets per thread
 JT = int(os.environ.get("RISE_ALLPAIRS_JT", "512"))  # sources per shared-memory tile
+UNROLL = int(os.environ.get("RISE_ALLPAIRS_UNROLL", "2"))  # source loop unroll
 
 
 def _split(body):
@@ -146,7 +147,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
             if a is None or streams.get(ld.buf, a) != a:
                 return None
             streams[ld.buf] = a
-    if not streams:
+    if not streams or any(prog.buffers[b].ctype != "float" for b in streams):
         return None
     s_list = sorted(streams.items())
     name = f"{base_name}_allpairs"
@@ -204,7 +205,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         ]
     lines += [
         "    __syncthreads();",
-        "#pragma unroll 2",
+        f"#pragma unroll {UNROLL}",
         "    for (int rs_jj = 0; rs_jj < rs_jn; ++rs_jj) {",
         "#pragma unroll",
         "      for (int rs_r = 0; rs_r < RS_RB; ++rs_r) {",

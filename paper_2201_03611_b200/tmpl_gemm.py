@@ -17,9 +17,17 @@ bound |C - C64| <= 2 K u (|A||B|) of SURVEY.md §8 d, not bit equality.
 
 from __future__ import annotations
 
+import os
+
 from . import lir
 from ._ref import nat
 from .emit_cuda import NatRenderer, kernel_head, py_expr
+
+# tile width, pipeline depth and whether the converter writes hi tiles back
+# (overridable for tuning sweeps only)
+BN = int(os.environ.get("RISE_GEMM_BN", "128"))
+STAGES = int(os.environ.get("RISE_GEMM_STAGES", "3"))
+WRITE_HI = os.environ.get("RISE_GEMM_WRITE_HI", "1") == "1"
 
 
 def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
@@ -62,10 +70,12 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
         return None
     name = f"{base_name}_gemm"
     r = NatRenderer(prog.clamps)
+    bn, stages, write_hi = BN, STAGES, WRITE_HI
     extra = ["const __grid_constant__ rs_tmap rs_mapA", "const __grid_constant__ rs_tmap rs_mapB"]
     lines = kernel_head(prog, name, temps, launch_bounds="192, 1", extra_params=extra)
     lines += [
-        f"  rise_gemm::gemm_3xtf32<{r(K)}>({st.target.buf}, {r(N)}, &rs_mapA, &rs_mapB);",
+        f"  rise_gemm::gemm_3xtf32<{r(K)}, {bn}, {stages}, {'true' if write_hi else 'false'}>"
+        f"({st.target.buf}, {r(N)}, &rs_mapA, &rs_mapB);",
         "}",
     ]
     plan = {
@@ -73,15 +83,16 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
         "kind": "gemm_tc",
         "M": py_expr(M),
         "N": py_expr(N),
+        "bn": bn,
         "fmad": False,
         "order": "3xtf32 tensor-core (reassociated)",
-        "pre": [f"({py_expr(M)}) % 128 == 0", f"({py_expr(N)}) % 128 == 0", f"({py_expr(K)}) % 32 == 0"],
-        "smem": 3 * 2 * (16384 + 16384) + 1024 + 256,
+        "pre": [f"({py_expr(M)}) % 128 == 0", f"({py_expr(N)}) % {bn} == 0", f"({py_expr(K)}) % 32 == 0"],
+        "smem": stages * 2 * (128 * 32 * 4 + bn * 32 * 4) + 1024 + 256,
         "extra_args": [
             {"kind": "tma2d", "buf": a_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(M)], "pitch": py_expr(K),
              "box": [32, 128], "swizzle": 3},
             {"kind": "tma2d", "buf": b_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(N)], "pitch": py_expr(K),
-             "box": [32, 128], "swizzle": 3},
+             "box": [32, bn], "swizzle": 3},
         ],
     }
     return "\n".join(lines) + "\n", plan
@@ -92,4 +103,4 @@ def launch(st, nats, sm):
 
     M = eval_py(st["M"], nats)
     N = eval_py(st["N"], nats)
-    return (N // 128, M // 128, 1), (192, 1, 1), st["smem"], (1, 1, 1)
+    return (N // st["bn"], M // 128, 1), (192, 1, 1), st["smem"], (1, 1, 1)

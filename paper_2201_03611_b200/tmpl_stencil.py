@@ -107,7 +107,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
             cur = tiled.setdefault(ld.buf, [r0[0], r0[1], r1[0], r1[1]])
             cur[0], cur[1] = min(cur[0], r0[0]), max(cur[1], r0[1])
             cur[2], cur[3] = min(cur[2], r1[0]), max(cur[3], r1[1])
-    if len(tiled) != 1:
+    if len(tiled) != 1 or any(prog.buffers[b].ctype != "float" for b in tiled):
         return None
     (abuf, (o0lo, o0hi, o1lo, o1hi)), = tiled.items()
     if not (o0lo <= 0 <= o0hi and o1lo <= 0 <= o1hi) or o0hi - o0lo > 8 or o1hi - o1lo > 8:

@@ -36,7 +36,7 @@ import os
 BLOCK = int(os.environ.get("RISE_ALLPAIRS_BLOCK", "64"))
 RB = int(os.environ.get("RISE_ALLPAIRS_RB", "2"))  # targets per thread
 JT = int(os.environ.get("RISE_ALLPAIRS_JT", "512"))  # sources per shared-memory tile
-UNROLL = int(os.environ.get("RISE_ALLPAIRS_UNROLL", "2"))  # source loop unroll
+UNROLL = int(os.environ.get("RISE_ALLPAIRS_UNROLL", "4"))  # source loop unroll
 
 
 def _split(body):
@@ -154,11 +154,19 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     r = NatRenderer(prog.clamps)
     fast = False  # fast math: FMA contraction + MUFU rsqrt
 
+    # sources are staged as array-of-records: one record of REC floats per
+    # source (e.g. x, y, z, m), 16-byte aligned, so a record is one LDS.128
+    offsets, rec = {}, 0
+    for buf, a in s_list:
+        offsets[buf] = rec
+        rec += a
+    rec = -(-rec // 4) * 4 if rec > 2 else rec
+
     def hook(ld):
         if ld.buf in streams and j in nat.free_vars(ld.index):
-            k = [b for b, _ in s_list].index(ld.buf)
             a = streams[ld.buf]
-            return f"rs_s{k}[({r(ld.index)}) - {a} * rs_j0]"
+            off = nat.normalize(ld.index - nat.Var(j) * nat.Const(a))
+            return f"rs_s[({j} - rs_j0) * {rec} + {offsets[ld.buf]} + ({r(off)})]"
         return None
 
     g = GenericKernel(prog, Stage("serial", jloop.body), "_", [], exact=fast)
@@ -173,8 +181,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     lines += [
         f"  constexpr int RS_NT = {r(NT)}, RS_NS = {r(NS)}, RS_JT = {JT}, RS_RB = {RB}, RS_C = {Cv};",
     ]
-    for k, (buf, a) in enumerate(s_list):
-        lines.append(f"  __shared__ float rs_s{k}[RS_JT * {a}];")
+    lines.append(f"  __shared__ __align__(16) float rs_s[RS_JT * {rec}];")
     lines += [
         f"  const int rs_g0 = blockIdx.x * ({BLOCK} * RS_RB) + threadIdx.x;",
         "  int rs_j0 = 0;",
@@ -185,9 +192,11 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         f"    return {acc.name};",
         "  };",
         f"  {acc.ctype} rs_acc[RS_RB][RS_C];",
+        "  int rs_gt[RS_RB];",
         "#pragma unroll",
         "  for (int rs_r = 0; rs_r < RS_RB; ++rs_r) {",
         f"    const int {gv} = min(rs_g0 + rs_r * {BLOCK}, RS_NT - 1);",
+        f"    rs_gt[rs_r] = {gv};",
         "#pragma unroll",
         "    for (int rs_c = 0; rs_c < RS_C; ++rs_c) {",
         f"      {cdecl} = rs_c;",
@@ -198,10 +207,10 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "    const int rs_jn = RS_NS - rs_j0 < RS_JT ? RS_NS - rs_j0 : RS_JT;",
         "    __syncthreads();",
     ]
-    for k, (buf, a) in enumerate(s_list):
+    for buf, a in s_list:
         lines += [
             f"    for (int rs_e = threadIdx.x; rs_e < rs_jn * {a}; rs_e += {BLOCK})",
-            f"      rs_s{k}[rs_e] = {buf}[{a} * rs_j0 + rs_e];",
+            f"      rs_s[(rs_e / {a}) * {rec} + {offsets[buf]} + rs_e % {a}] = {buf}[{a} * rs_j0 + rs_e];",
         ]
     lines += [
         "    __syncthreads();",
@@ -209,10 +218,9 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "    for (int rs_jj = 0; rs_jj < rs_jn; ++rs_jj) {",
         "#pragma unroll",
         "      for (int rs_r = 0; rs_r < RS_RB; ++rs_r) {",
-        f"        const int rs_g = min(rs_g0 + rs_r * {BLOCK}, RS_NT - 1);",
         "#pragma unroll",
         "        for (int rs_c = 0; rs_c < RS_C; ++rs_c)",
-        "          rs_acc[rs_r][rs_c] = rs_step(rs_g, rs_c, rs_j0 + rs_jj, rs_acc[rs_r][rs_c]);",
+        "          rs_acc[rs_r][rs_c] = rs_step(rs_gt[rs_r], rs_c, rs_j0 + rs_jj, rs_acc[rs_r][rs_c]);",
         "      }",
         "    }",
         "  }",

@@ -25,9 +25,9 @@ from .emit_cuda import NatRenderer, kernel_head, py_expr
 
 # tile width, pipeline depth and whether the converter writes hi tiles back
 # (overridable for tuning sweeps only)
-BN = int(os.environ.get("RISE_GEMM_BN", "128"))
-STAGES = int(os.environ.get("RISE_GEMM_STAGES", "3"))
-WRITE_HI = os.environ.get("RISE_GEMM_WRITE_HI", "1") == "1"
+BN = int(os.environ.get("RISE_GEMM_BN", "256"))
+STAGES = int(os.environ.get("RISE_GEMM_STAGES", "2"))
+WRITE_HI = os.environ.get("RISE_GEMM_WRITE_HI", "0") == "1"
 
 
 def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):

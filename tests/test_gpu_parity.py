@@ -183,3 +183,31 @@ def test_sgemm_falls_back_when_tiles_do_not_divide(gpu):
     Bt = oracle.rng_inputs(5, 36, 24)
     got = run_cuda(code, c.unit, {"n": 100, "m": 36, "k": 24}, [A, Bt], as_numpy=True).reshape(100, 36)
     np.testing.assert_array_equal(got, oracle.sgemm_bt(A, Bt))
+
+
+def test_tensor_core_ignores_low_tf32_bits(gpu):
+    """gemm_tc skips writing the hi tiles back: the tcgen05 kind::tf32 datapath
+    ignores the low 13 mantissa bits of each fp32 operand, so raw x acts as
+    hi.  Guard that assumption: both variants must agree bit for bit."""
+    import subprocess
+    import sys
+
+    code = (
+        "import os, sys, numpy as np; sys.path.insert(0, 'oracle'); import oracle;"
+        "from paper_2201_03611_b200 import compile_program, emit_cuda, programs, run_cuda;"
+        "c = compile_program(programs.SGEMM_BT, None, name='sgemm');"
+        "A = oracle.rng_inputs(4, 256, 256); B = oracle.rng_inputs(5, 256, 256);"
+        "out = run_cuda(emit_cuda(c.unit), c.unit, {'n': 256, 'm': 256, 'k': 256}, [A, B], as_numpy=True);"
+        "np.save(sys.argv[1], out)"
+    )
+    import os
+    import tempfile
+
+    outs = []
+    for hi in ("0", "1"):
+        path = os.path.join(tempfile.mkdtemp(), "out.npy")
+        env = dict(os.environ, RISE_GEMM_WRITE_HI=hi, RISE_GEMM_BN="128", RISE_GEMM_STAGES="3")
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=env,
+                       cwd=str(__import__("pathlib").Path(__file__).resolve().parent.parent))
+        outs.append(np.load(path))
+    np.testing.assert_array_equal(outs[0], outs[1])

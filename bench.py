@@ -510,15 +510,29 @@ def _distributed_step(wl, exe, dev_in, out, stream, dist, rank, world):
         m = exe.nats["m"]
         local = img.view(-1, m)
 
+        host_staged = dist.get_backend() != "nccl"  # gloo P2P moves CPU tensors only (test path)
+        stage = torch.empty((4, m), dtype=torch.float32) if host_staged else None
+
         def step():
             with torch.cuda.stream(stream):
+                if host_staged:
+                    stage[0].copy_(local[1])
+                    stage[1].copy_(local[-2])
+                    send_top, send_bot, recv_top, recv_bot = stage[0], stage[1], stage[2], stage[3]
+                else:
+                    send_top, send_bot, recv_top, recv_bot = local[1], local[-2], local[0], local[-1]
                 ops = []
                 if rank > 0:
-                    ops += [dist.P2POp(dist.isend, local[1], rank - 1), dist.P2POp(dist.irecv, local[0], rank - 1)]
+                    ops += [dist.P2POp(dist.isend, send_top, rank - 1), dist.P2POp(dist.irecv, recv_top, rank - 1)]
                 if rank < world - 1:
-                    ops += [dist.P2POp(dist.isend, local[-2], rank + 1), dist.P2POp(dist.irecv, local[-1], rank + 1)]
+                    ops += [dist.P2POp(dist.isend, send_bot, rank + 1), dist.P2POp(dist.irecv, recv_bot, rank + 1)]
                 for req in dist.batch_isend_irecv(ops):
                     req.wait()
+                if host_staged:
+                    if rank > 0:
+                        local[0].copy_(recv_top)
+                    if rank < world - 1:
+                        local[-1].copy_(recv_bot)
             exe(*dev_in, out=out, stream=stream)
 
         return step

@@ -90,7 +90,7 @@ def nbodyShard = depFun((t: Nat, n: Nat) =>
              acc + (fst(q) - fst(snd(col))) *
                (snd(snd(q)) *
                  ((zip(fst(snd(q)))(fst(pv)) |> reduceSeq(Private)(fun(r2, d => r2 + (fst(d) - snd(d)) * (fst(d) - snd(d))))(0.01f))
-                   |> fun(r2 => rsqrt(r2) * rsqrt(r2) * rsqrt(r2)))) ))(0.0f)) )) )) ))))))
+                   |> fun(r2 => rsqrt(r2) * rsqrt(r2) * rsqrt(r2)))) ))(0.0f)) )) )) )))))
 """
 
 CONFIGS = {

@@ -211,3 +211,16 @@ def test_tensor_core_ignores_low_tf32_bits(gpu):
                        cwd=str(__import__("pathlib").Path(__file__).resolve().parent.parent))
         outs.append(np.load(path))
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+def test_nbody_shard_program_equals_full_rows(gpu):
+    """The per-GPU program of the multi-GPU decomposition (a target block
+    against all sources) reproduces the single-GPU rows bit for bit."""
+    n, t0, t = 4096, 1024, 512
+    pos, vel, mass = _nbody_inputs(n)
+    full = compile_program(programs.NBODY, None, name="nbody")
+    ref = run_cuda(emit_cuda(full.unit), full.unit, {"n": n}, [pos, vel, mass], as_numpy=True).reshape(n, 3)
+    part = compile_program(programs.NBODY_SHARD, None, name="nbodyShard")
+    got = run_cuda(emit_cuda(part.unit), part.unit, {"t": t, "n": n},
+                   [pos[t0:t0 + t], vel[t0:t0 + t], pos, mass], as_numpy=True).reshape(t, 3)
+    np.testing.assert_array_equal(got, ref[t0:t0 + t])

@@ -26,6 +26,13 @@ RS_DEVICE float rs_rsqrt_fast(float x) {
   return y;
 }
 
+// packed fp32x2 helpers (FFMA2 / FADD2 / FMUL2 are sm_100 instructions)
+RS_DEVICE float2 rs_bcast2(float x) { return make_float2(x, x); }
+RS_DEVICE float2 rs_neg2(float2 a) { return make_float2(-a.x, -a.y); }
+RS_DEVICE float2 rs_div2(float2 a, float2 b) { return make_float2(a.x / b.x, a.y / b.y); }
+RS_DEVICE float2 rs_rsqrt2(float2 a) { return make_float2(rs_rsqrt_fast(a.x), rs_rsqrt_fast(a.y)); }
+RS_DEVICE float2 rs_sqrt2(float2 a) { return make_float2(sqrtf(a.x), sqrtf(a.y)); }
+
 RS_DEVICE unsigned rs_smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }

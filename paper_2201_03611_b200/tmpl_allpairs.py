@@ -37,6 +37,7 @@ BLOCK = int(os.environ.get("RISE_ALLPAIRS_BLOCK", "64"))
 RB = int(os.environ.get("RISE_ALLPAIRS_RB", "2"))  # targets per thread
 JT = int(os.environ.get("RISE_ALLPAIRS_JT", "512"))  # sources per shared-memory tile
 UNROLL = int(os.environ.get("RISE_ALLPAIRS_UNROLL", "4"))  # source loop unroll
+PACKED = os.environ.get("RISE_ALLPAIRS_PACKED", "1") == "1"  # two targets per FFMA2/FADD2/FMUL2
 
 
 def _split(body):
@@ -172,6 +173,13 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     g = GenericKernel(prog, Stage("serial", jloop.body), "_", [], exact=fast)
     g.r = ValueRenderer(prog, exact=fast, load_hook=hook)
     step_lines = g.thread(jloop.body, 2)
+    packed = PACKED and RB % 2 == 0 and acc.ctype == "float"
+    step2_lines = None
+    if packed:
+        try:
+            step2_lines = _Vec2(prog, gv, hook).stmt(jloop.body, 2)
+        except _NoVec2:
+            packed = False
     gp = GenericKernel(prog, Stage("serial", lir.Seq(list(post))), "_", [], exact=fast)
     post_lines = gp.thread(lir.Seq(list(post)), 3)
     vinit = ValueRenderer(prog, exact=fast)(init.value)
@@ -191,6 +199,14 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     lines += [
         f"    return {acc.name};",
         "  };",
+    ]
+    if packed:
+        # the same step for two targets at once, in packed fp32x2 arithmetic
+        lines.append(f"  auto rs_step2 = [&](const int rs_ga, const int rs_gb, {cdecl}, const int {j}, "
+                     f"float2 {acc.name}) -> float2 {{")
+        lines += step2_lines
+        lines += [f"    return {acc.name};", "  };"]
+    lines += [
         f"  {acc.ctype} rs_acc[RS_RB][RS_C];",
         "  int rs_gt[RS_RB];",
         "#pragma unroll",
@@ -212,18 +228,39 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
             f"    for (int rs_e = threadIdx.x; rs_e < rs_jn * {a}; rs_e += {BLOCK})",
             f"      rs_s[(rs_e / {a}) * {rec} + {offsets[buf]} + rs_e % {a}] = {buf}[{a} * rs_j0 + rs_e];",
         ]
+    if packed:
+        lines += [
+            "    __syncthreads();",
+            f"#pragma unroll {UNROLL}",
+            "    for (int rs_jj = 0; rs_jj < rs_jn; ++rs_jj) {",
+            "#pragma unroll",
+            "      for (int rs_p = 0; rs_p < RS_RB / 2; ++rs_p) {",
+            "#pragma unroll",
+            "        for (int rs_c = 0; rs_c < RS_C; ++rs_c) {",
+            "          float2 rs_a2 = make_float2(rs_acc[2 * rs_p][rs_c], rs_acc[2 * rs_p + 1][rs_c]);",
+            "          rs_a2 = rs_step2(rs_gt[2 * rs_p], rs_gt[2 * rs_p + 1], rs_c, rs_j0 + rs_jj, rs_a2);",
+            "          rs_acc[2 * rs_p][rs_c] = rs_a2.x;",
+            "          rs_acc[2 * rs_p + 1][rs_c] = rs_a2.y;",
+            "        }",
+            "      }",
+            "    }",
+            "  }",
+        ]
+    else:
+        lines += [
+            "    __syncthreads();",
+            f"#pragma unroll {UNROLL}",
+            "    for (int rs_jj = 0; rs_jj < rs_jn; ++rs_jj) {",
+            "#pragma unroll",
+            "      for (int rs_r = 0; rs_r < RS_RB; ++rs_r) {",
+            "#pragma unroll",
+            "        for (int rs_c = 0; rs_c < RS_C; ++rs_c)",
+            "          rs_acc[rs_r][rs_c] = rs_step(rs_gt[rs_r], rs_c, rs_j0 + rs_jj, rs_acc[rs_r][rs_c]);",
+            "      }",
+            "    }",
+            "  }",
+        ]
     lines += [
-        "    __syncthreads();",
-        f"#pragma unroll {UNROLL}",
-        "    for (int rs_jj = 0; rs_jj < rs_jn; ++rs_jj) {",
-        "#pragma unroll",
-        "      for (int rs_r = 0; rs_r < RS_RB; ++rs_r) {",
-        "#pragma unroll",
-        "        for (int rs_c = 0; rs_c < RS_C; ++rs_c)",
-        "          rs_acc[rs_r][rs_c] = rs_step(rs_gt[rs_r], rs_c, rs_j0 + rs_jj, rs_acc[rs_r][rs_c]);",
-        "      }",
-        "    }",
-        "  }",
         "#pragma unroll",
         "  for (int rs_r = 0; rs_r < RS_RB; ++rs_r) {",
         f"    const int {gv} = rs_g0 + rs_r * {BLOCK};",
@@ -246,6 +283,107 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "pre": [],
     }
     return "\n".join(lines) + "\n", plan
+
+
+class _NoVec2(Exception):
+    pass
+
+
+class _Vec2:
+    """Render the fold body for two targets at once: every f32 value becomes a
+    float2 (lane x = target a, lane y = target b); target-dependent loads are
+    gathered per lane, everything else is broadcast; `a*b + c` patterns become
+    one FFMA2 (the same contraction the scalar fast path allows)."""
+
+    def __init__(self, prog, gv, hook):
+        self.prog = prog
+        self.hook = hook
+        self.gv = gv
+        self.ra = NatRenderer(prog.clamps, names={gv: "rs_ga"})
+        self.rb = NatRenderer(prog.clamps, names={gv: "rs_gb"})
+        self.r = NatRenderer(prog.clamps)
+        self.scalar_inputs = {n for n, b in prog.inputs if isinstance(b, lir.ScalarRef)}
+        self.local_arrays = set()
+
+    def val(self, e):
+        if isinstance(e, lir.Lit):
+            if e.ctype != "float":
+                raise _NoVec2()
+            return f"make_float2({e.text}, {e.text})"
+        if isinstance(e, lir.ScalarRef):
+            if e.ctype != "float":
+                raise _NoVec2()
+            if e.name in self.scalar_inputs:
+                return f"make_float2({e.name}, {e.name})"
+            return e.name
+        if isinstance(e, lir.Load):
+            if e.ctype != "float":
+                raise _NoVec2()
+            if e.buf in self.local_arrays:
+                return f"{e.buf}[{self.r(e.index)}]"
+            h = self.hook(e)
+            if h is not None:
+                return f"rs_bcast2({h})"
+            if self.gv in nat.free_vars(e.index):
+                return f"make_float2({e.buf}[{self.ra(e.index)}], {e.buf}[{self.rb(e.index)}])"
+            return f"rs_bcast2({e.buf}[{self.r(e.index)}])"
+        if isinstance(e, lir.Bin):
+            if e.ctype != "float":
+                raise _NoVec2()
+            if e.op == "+":
+                if isinstance(e.b, lir.Bin) and e.b.op == "*":
+                    return f"__ffma2_rn({self.val(e.b.a)}, {self.val(e.b.b)}, {self.val(e.a)})"
+                if isinstance(e.a, lir.Bin) and e.a.op == "*":
+                    return f"__ffma2_rn({self.val(e.a.a)}, {self.val(e.a.b)}, {self.val(e.b)})"
+                return f"__fadd2_rn({self.val(e.a)}, {self.val(e.b)})"
+            if e.op == "-":
+                if isinstance(e.a, lir.Bin) and e.a.op == "*":
+                    return f"__ffma2_rn({self.val(e.a.a)}, {self.val(e.a.b)}, rs_neg2({self.val(e.b)}))"
+                return f"__fadd2_rn({self.val(e.a)}, rs_neg2({self.val(e.b)}))"
+            if e.op == "*":
+                return f"__fmul2_rn({self.val(e.a)}, {self.val(e.b)})"
+            if e.op == "/":
+                return f"rs_div2({self.val(e.a)}, {self.val(e.b)})"
+        if isinstance(e, lir.Un):
+            if e.fn == "rsqrt":
+                return f"rs_rsqrt2({self.val(e.a)})"
+            if e.fn == "sqrt":
+                return f"rs_sqrt2({self.val(e.a)})"
+        raise _NoVec2()
+
+    def stmt(self, s, ind):
+        p = "  " * ind
+        if isinstance(s, lir.Seq):
+            out = []
+            for c in s.stmts:
+                out += self.stmt(c, ind)
+            return out
+        if isinstance(s, lir.Alloc):
+            if s.ctype != "float":
+                raise _NoVec2()
+            if s.dims:
+                self.local_arrays.add(s.name)
+                size = nat.Const(1)
+                for d in s.dims:
+                    size = size * d
+                decl = f"{p}float2 {s.name}[{self.r(nat.normalize(size))}];"
+            else:
+                decl = f"{p}float2 {s.name};"
+            return [decl] + self.stmt(s.body, ind)
+        if isinstance(s, lir.Assign):
+            t = s.target
+            if isinstance(t, lir.ScalarRef):
+                lhs = t.name
+            elif isinstance(t, lir.Store) and t.buf in self.local_arrays:
+                lhs = f"{t.buf}[{self.r(t.index)}]"
+            else:
+                raise _NoVec2()
+            return [f"{p}{lhs} = {self.val(s.value)};"]
+        if isinstance(s, lir.For):
+            pre = ["#pragma unroll"] if isinstance(s.bound, nat.Const) and s.bound.value <= 16 else []
+            head = f"{p}for (int {s.var} = 0; {s.var} < {self.r(s.bound)}; {s.var} += 1) {{"
+            return pre + [head] + self.stmt(s.body, ind + 1) + [f"{p}}}"]
+        raise _NoVec2()
 
 
 def launch(st, nats, sm):

@@ -153,6 +153,33 @@ class Executable:
                 args.append(self._extra_arg(extra, buffers, temps))
             fn.launch(grid, block, args, smem=smem, stream=stream, cluster=cluster)
 
+    def bind(self, buffers: dict, stream=None):
+        """Pre-build every launch (argument arrays, tensor maps) for fixed
+        buffers; the returned callable just issues rs_launch per stage —
+        the low-overhead path for repeated steps (benchmarks, CUDA graphs)."""
+        temps = self.temps()
+        scalar_types = {i["name"]: i["ctype"] for i in self.plan["inputs"] if i["scalar"]}
+        base_args = []
+        for name in self.plan["args"]:
+            if name in temps:
+                base_args.append(ctypes.c_void_p(temps[name].data_ptr()))
+            elif name in scalar_types:
+                v = buffers[name]
+                base_args.append(ctypes.c_float(float(v)) if scalar_types[name] == "float" else ctypes.c_int(int(v)))
+            else:
+                base_args.append(ctypes.c_void_p(_dptr(buffers[name])))
+        prepared = []
+        for st, fn, grid, block, smem, cluster in self.kernels:
+            args = list(base_args) + [self._extra_arg(e, buffers, temps) for e in st.get("extra_args", [])]
+            prepared.append(rt.PreparedLaunch(fn, grid, block, args, smem, stream, cluster))
+
+        def launch_all():
+            for p in prepared:
+                p()
+
+        launch_all.prepared = prepared
+        return launch_all
+
     def _extra_arg(self, extra, buffers, temps):
         kind = extra["kind"]
         if kind == "workspace":

@@ -228,6 +228,27 @@ class Function:
         )
 
 
+class PreparedLaunch:
+    """One kernel launch with its argument array built once."""
+
+    def __init__(self, fn: Function, grid, block, args, smem=0, stream=None, cluster=(1, 1, 1)):
+        self.fn = fn
+        self.args = list(args)  # keep the ctypes values alive
+        self.g = (ctypes.c_uint * 3)(*_dim3(grid))
+        self.b = (ctypes.c_uint * 3)(*_dim3(block))
+        self.c = (ctypes.c_uint * 3)(*_dim3(cluster))
+        self.ptrs = (ctypes.c_void_p * max(1, len(self.args)))()
+        for k, a in enumerate(self.args):
+            self.ptrs[k] = ctypes.cast(ctypes.byref(a), ctypes.c_void_p)
+        self.smem = int(smem)
+        self.stream = _stream_ptr(stream)
+        self._launch = lib().rs_launch
+
+    def __call__(self):
+        if self._launch(self.fn.handle, self.g, self.b, self.c, self.smem, self.stream, self.ptrs) != 0:
+            check_run(1, f"launch of {self.fn.name}")
+
+
 def _dim3(d):
     if isinstance(d, int):
         return (d, 1, 1)

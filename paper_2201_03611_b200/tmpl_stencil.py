@@ -35,6 +35,7 @@ TX, TY = 32, 8
 RPT = 8  # output rows per thread
 CPT = 4  # adjacent output columns per thread
 TR, TC = TY * RPT, TX * CPT
+BLOCKS_PER_SM = 2  # persistent blocks per SM (2 x two 36 KB stages)
 
 
 def _seq_loop_bounds(stmt):
@@ -157,28 +158,35 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         f"  constexpr int RS_R = {r(R)}, RS_C = {r(C)};",
         f"  constexpr int RS_H = {r(A.dims[0])}, RS_W = {r(A.dims[1])};",
         f"  constexpr int RS_SR = {sr}, RS_SW = {sw};",
-        "  __shared__ __align__(128) float rs_tile[RS_SR * RS_SW];",
-        "  __shared__ __align__(8) unsigned long long rs_bar;",
-        f"  const int rs_r0 = blockIdx.y * {TR}, rs_c0 = blockIdx.x * {TC};",
-        f"  const int rs_tr0 = rs_r0 + ({o0lo}), rs_tc0 = rs_c0 - {lp};",
+        f"  constexpr int RS_NTX = (RS_C + {TC - 1}) / {TC}, RS_NTY = (RS_R + {TR - 1}) / {TR};",
+        "  constexpr int RS_NTILES = RS_NTX * RS_NTY;",
+        "  extern __shared__ __align__(128) unsigned char rs_dsmem[];",
+        "  float* rs_buf = reinterpret_cast<float*>(rs_dsmem + ((128u - (rs_smem_addr(rs_dsmem) & 127u)) & 127u));",
+        "  unsigned long long* rs_bar = reinterpret_cast<unsigned long long*>(rs_buf + 2 * RS_SR * RS_SW);",
         "  const int rs_tid = threadIdx.y * blockDim.x + threadIdx.x;",
-        "  const bool rs_interior = rs_tr0 >= 0 && rs_tr0 + RS_SR <= RS_H && rs_tc0 >= 0 && rs_tc0 + RS_SW <= RS_W;",
-        "  if (rs_interior) {",
-        "    if (rs_tid == 0) {",
-        "      rs_mbar_init(&rs_bar, 1);",
-        "      rs_fence_barrier_init();",
-        "      rs_mbar_arrive_expect_tx(&rs_bar, (unsigned)(RS_SR * RS_SW * 4));",
-        "      rs_tma_load_2d(rs_tile, &rs_map, rs_tc0, rs_tr0, &rs_bar);",
-        "    }",
-        "    __syncthreads();",
-        "    rs_mbar_wait(&rs_bar, 0u);",
-        "  } else {",
-        f"    for (int rs_e = rs_tid; rs_e < RS_SR * RS_SW; rs_e += {TX * TY}) {{",
-        "      const int rs_y = rs_e / RS_SW, rs_x = rs_e - (rs_e / RS_SW) * RS_SW;",
-        f"      rs_tile[rs_e] = {abuf}[rs_clamp(rs_tr0 + rs_y, {hdim}) * RS_W + rs_clamp(rs_tc0 + rs_x, {wdim})];",
-        "    }",
-        "    __syncthreads();",
+        "  // tile t -> (rs_r0, rs_c0); interior tiles arrive by TMA, border tiles by clamped loads",
+        "  auto rs_origin = [&](int t, int& r0, int& c0) {",
+        f"    r0 = (t / RS_NTX) * {TR}; c0 = (t % RS_NTX) * {TC};",
+        "  };",
+        "  auto rs_is_interior = [&](int r0, int c0) {",
+        f"    const int tr0 = r0 + ({o0lo}), tc0 = c0 - {lp};",
+        "    return tr0 >= 0 && tr0 + RS_SR <= RS_H && tc0 >= 0 && tc0 + RS_SW <= RS_W;",
+        "  };",
+        "  auto rs_issue = [&](int t, int s) {  // thread 0 only",
+        "    int r0, c0;",
+        "    rs_origin(t, r0, c0);",
+        "    if (!rs_is_interior(r0, c0)) return;",
+        "    rs_fence_proxy_async();  // earlier generic-proxy accesses of this stage precede the TMA write",
+        "    rs_mbar_arrive_expect_tx(&rs_bar[s], (unsigned)(RS_SR * RS_SW * 4));",
+        f"    rs_tma_load_2d(rs_buf + s * RS_SR * RS_SW, &rs_map, c0 - {lp}, r0 + ({o0lo}), &rs_bar[s]);",
+        "  };",
+        "  if (rs_tid == 0) {",
+        "    rs_mbar_init(&rs_bar[0], 1);",
+        "    rs_mbar_init(&rs_bar[1], 1);",
+        "    rs_fence_barrier_init();",
+        "    if ((int)blockIdx.x < RS_NTILES) rs_issue(blockIdx.x, 0);",
         "  }",
+        "  __syncthreads();",
     ]
     for buf, size in sorted(small.items()):
         lines += [
@@ -187,41 +195,63 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
             f"  for (int rs_e = 0; rs_e < {size}; ++rs_e) rs_p_{buf}[rs_e] = __ldg({buf} + rs_e);",
         ]
     lines += [
-        "  // this thread's register window (tile rows ty*RPT.., columns lp + tx*CPT - hcl..)",
-        f"  float rs_v[{wr}][{wc}];",
+        "  unsigned rs_phase0 = 0u, rs_phase1 = 0u;",
+        "  int rs_it = 0;",
+        "  for (int rs_t = blockIdx.x; rs_t < RS_NTILES; rs_t += gridDim.x, ++rs_it) {",
+        "    const int rs_s = rs_it & 1;",
+        "    int rs_r0, rs_c0;",
+        "    rs_origin(rs_t, rs_r0, rs_c0);",
+        f"    const int rs_tr0 = rs_r0 + ({o0lo}), rs_tc0 = rs_c0 - {lp};",
+        "    float* rs_tile = rs_buf + rs_s * RS_SR * RS_SW;",
+        "    // prefetch the next tile into the other stage (freed by the barrier that ended the previous tile)",
+        "    if (rs_tid == 0 && rs_t + (int)gridDim.x < RS_NTILES) rs_issue(rs_t + gridDim.x, rs_s ^ 1);",
+        "    if (rs_is_interior(rs_r0, rs_c0)) {",
+        "      if (rs_s == 0) { rs_mbar_wait(&rs_bar[0], rs_phase0); rs_phase0 ^= 1u; }",
+        "      else { rs_mbar_wait(&rs_bar[1], rs_phase1); rs_phase1 ^= 1u; }",
+        "    } else {",
+        f"      for (int rs_e = rs_tid; rs_e < RS_SR * RS_SW; rs_e += {TX * TY}) {{",
+        "        const int rs_y = rs_e / RS_SW, rs_x = rs_e - (rs_e / RS_SW) * RS_SW;",
+        f"        rs_tile[rs_e] = {abuf}[rs_clamp(rs_tr0 + rs_y, {hdim}) * RS_W + rs_clamp(rs_tc0 + rs_x, {wdim})];",
+        "      }",
+        "      __syncthreads();",
+        "    }",
+        "    // this thread's register window (tile rows ty*RPT.., columns lp + tx*CPT - hcl..)",
+        f"    float rs_v[{wr}][{wc}];",
         "#pragma unroll",
-        f"  for (int rs_y = 0; rs_y < {wr}; ++rs_y) {{",
-        f"    const float* rs_row = rs_tile + (threadIdx.y * {RPT} + rs_y) * RS_SW + {lp} + threadIdx.x * {CPT};",
-        "    const float4 rs_mid = *reinterpret_cast<const float4*>(rs_row);",
+        f"    for (int rs_y = 0; rs_y < {wr}; ++rs_y) {{",
+        f"      const float* rs_row = rs_tile + (threadIdx.y * {RPT} + rs_y) * RS_SW + {lp} + threadIdx.x * {CPT};",
+        "      const float4 rs_mid = *reinterpret_cast<const float4*>(rs_row);",
     ]
     for k in range(hcl):
-        lines.append(f"    rs_v[rs_y][{k}] = rs_row[{k - hcl}];")
+        lines.append(f"      rs_v[rs_y][{k}] = rs_row[{k - hcl}];")
     lines += [
-        f"    rs_v[rs_y][{hcl}] = rs_mid.x; rs_v[rs_y][{hcl + 1}] = rs_mid.y;",
-        f"    rs_v[rs_y][{hcl + 2}] = rs_mid.z; rs_v[rs_y][{hcl + 3}] = rs_mid.w;",
+        f"      rs_v[rs_y][{hcl}] = rs_mid.x; rs_v[rs_y][{hcl + 1}] = rs_mid.y;",
+        f"      rs_v[rs_y][{hcl + 2}] = rs_mid.z; rs_v[rs_y][{hcl + 3}] = rs_mid.w;",
     ]
     for k in range(hcr):
-        lines.append(f"    rs_v[rs_y][{hcl + CPT + k}] = rs_row[{CPT + k}];")
+        lines.append(f"      rs_v[rs_y][{hcl + CPT + k}] = rs_row[{CPT + k}];")
     lines += [
-        "  }",
+        "    }",
+        "    __syncthreads();  // the stage may be refilled once every thread holds its window",
     ]
     for guarded in (False, True):
         if not guarded:
-            lines.append(f"  if (rs_r0 + {TR} <= RS_R && rs_c0 + {TC} <= RS_C) {{")
+            lines.append(f"    if (rs_r0 + {TR} <= RS_R && rs_c0 + {TC} <= RS_C) {{")
         else:
-            lines.append("  } else {")
+            lines.append("    } else {")
         lines += [
             "#pragma unroll",
-            f"  for (int rs_k = 0; rs_k < {RPT}; ++rs_k) {{",
+            f"    for (int rs_k = 0; rs_k < {RPT}; ++rs_k) {{",
             "#pragma unroll",
-            f"    for (int rs_q = 0; rs_q < {CPT}; ++rs_q) {{",
-            f"      const int {rv} = rs_r0 + threadIdx.y * {RPT} + rs_k;",
-            f"      const int {cv} = rs_c0 + threadIdx.x * {CPT} + rs_q;",
-            f"      if ({'true' if not guarded else f'{rv} < RS_R && {cv} < RS_C'}) {{",
+            f"      for (int rs_q = 0; rs_q < {CPT}; ++rs_q) {{",
+            f"        const int {rv} = rs_r0 + threadIdx.y * {RPT} + rs_k;",
+            f"        const int {cv} = rs_c0 + threadIdx.x * {CPT} + rs_q;",
+            f"        if ({'true' if not guarded else f'{rv} < RS_R && {cv} < RS_C'}) {{",
         ]
-        lines += body_lines
-        lines += ["      }", "    }", "  }"]
-    lines += ["  }", "}"]
+        lines += ["  " + x for x in body_lines]
+        lines += ["        }", "      }", "    }"]
+    lines += ["    }", "  }", "}"]
+    smem = 2 * sr * sw * 4 + 16 + 128
     plan = {
         "name": name,
         "kind": "stencil2d",
@@ -229,6 +259,8 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "cols": py_expr(C),
         "tile": [TR, TC],
         "block": [TX, TY],
+        "smem": smem,
+        "blocks_per_sm": BLOCKS_PER_SM,
         "fmad": False,
         "order": "preserved",
         "pre": [f"({py_expr(A.dims[1])}) % 4 == 0"],
@@ -245,4 +277,6 @@ def launch(st, nats, sm):
     rows = eval_py(st["rows"], nats)
     cols = eval_py(st["cols"], nats)
     tr, tc = st["tile"]
-    return (-(-cols // tc), -(-rows // tr), 1), (st["block"][0], st["block"][1], 1), 0, (1, 1, 1)
+    tiles = -(-cols // tc) * -(-rows // tr)
+    grid = max(1, min(tiles, sm * st.get("blocks_per_sm", 2)))  # persistent, tile-strided
+    return (grid, 1, 1), (st["block"][0], st["block"][1], 1), st.get("smem", 0), (1, 1, 1)

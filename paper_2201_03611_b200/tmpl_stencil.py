@@ -158,11 +158,12 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         f"  constexpr int RS_R = {r(R)}, RS_C = {r(C)};",
         f"  constexpr int RS_H = {r(A.dims[0])}, RS_W = {r(A.dims[1])};",
         f"  constexpr int RS_SR = {sr}, RS_SW = {sw};",
+        "  constexpr int RS_STAGE = (RS_SR * RS_SW + 31) / 32 * 32;  // stages stay 128-byte aligned (TMA)",
         f"  constexpr int RS_NTX = (RS_C + {TC - 1}) / {TC}, RS_NTY = (RS_R + {TR - 1}) / {TR};",
         "  constexpr int RS_NTILES = RS_NTX * RS_NTY;",
         "  extern __shared__ __align__(128) unsigned char rs_dsmem[];",
         "  float* rs_buf = reinterpret_cast<float*>(rs_dsmem + ((128u - (rs_smem_addr(rs_dsmem) & 127u)) & 127u));",
-        "  unsigned long long* rs_bar = reinterpret_cast<unsigned long long*>(rs_buf + 2 * RS_SR * RS_SW);",
+        "  unsigned long long* rs_bar = reinterpret_cast<unsigned long long*>(rs_buf + 2 * RS_STAGE);",
         "  const int rs_tid = threadIdx.y * blockDim.x + threadIdx.x;",
         "  // tile t -> (rs_r0, rs_c0); interior tiles arrive by TMA, border tiles by clamped loads",
         "  auto rs_origin = [&](int t, int& r0, int& c0) {",
@@ -178,7 +179,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "    if (!rs_is_interior(r0, c0)) return;",
         "    rs_fence_proxy_async();  // earlier generic-proxy accesses of this stage precede the TMA write",
         "    rs_mbar_arrive_expect_tx(&rs_bar[s], (unsigned)(RS_SR * RS_SW * 4));",
-        f"    rs_tma_load_2d(rs_buf + s * RS_SR * RS_SW, &rs_map, c0 - {lp}, r0 + ({o0lo}), &rs_bar[s]);",
+        f"    rs_tma_load_2d(rs_buf + s * RS_STAGE, &rs_map, c0 - {lp}, r0 + ({o0lo}), &rs_bar[s]);",
         "  };",
         "  if (rs_tid == 0) {",
         "    rs_mbar_init(&rs_bar[0], 1);",
@@ -202,7 +203,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "    int rs_r0, rs_c0;",
         "    rs_origin(rs_t, rs_r0, rs_c0);",
         f"    const int rs_tr0 = rs_r0 + ({o0lo}), rs_tc0 = rs_c0 - {lp};",
-        "    float* rs_tile = rs_buf + rs_s * RS_SR * RS_SW;",
+        "    float* rs_tile = rs_buf + rs_s * RS_STAGE;",
         "    // prefetch the next tile into the other stage (freed by the barrier that ended the previous tile)",
         "    if (rs_tid == 0 && rs_t + (int)gridDim.x < RS_NTILES) rs_issue(rs_t + gridDim.x, rs_s ^ 1);",
         "    if (rs_is_interior(rs_r0, rs_c0)) {",
@@ -251,7 +252,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         lines += ["  " + x for x in body_lines]
         lines += ["        }", "      }", "    }"]
     lines += ["    }", "  }", "}"]
-    smem = 2 * sr * sw * 4 + 16 + 128
+    smem = 2 * (-(-(sr * sw) // 32) * 32) * 4 + 16 + 128
     plan = {
         "name": name,
         "kind": "stencil2d",

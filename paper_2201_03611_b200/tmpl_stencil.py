@@ -35,7 +35,10 @@ TX, TY = 32, 8
 RPT = 8  # output rows per thread
 CPT = 4  # adjacent output columns per thread
 TR, TC = TY * RPT, TX * CPT
-BLOCKS_PER_SM = 2  # persistent blocks per SM (2 x two 36 KB stages)
+import os  # noqa: E402
+
+# persistent blocks per SM (each holds two 36 KB stages); overridable for sweeps
+BLOCKS_PER_SM = int(os.environ.get("RISE_STENCIL_BPS", "3"))
 
 
 def _seq_loop_bounds(stmt):

@@ -33,8 +33,8 @@ import os
 
 # 64-thread blocks x 2 targets per thread: 1024 blocks for 131072 bodies, so
 # the per-SM load is balanced to ~1% and each SM holds ~14 warps
-BLOCK = int(os.environ.get("RISE_ALLPAIRS_BLOCK", "64"))
-RB = int(os.environ.get("RISE_ALLPAIRS_RB", "2"))  # targets per thread
+BLOCK = int(os.environ.get("RISE_ALLPAIRS_BLOCK", "32"))
+RB = int(os.environ.get("RISE_ALLPAIRS_RB", "4"))  # targets per thread
 JT = int(os.environ.get("RISE_ALLPAIRS_JT", "512"))  # sources per shared-memory tile
 UNROLL = int(os.environ.get("RISE_ALLPAIRS_UNROLL", "4"))  # source loop unroll
 PACKED = os.environ.get("RISE_ALLPAIRS_PACKED", "1") == "1"  # two targets per FFMA2/FADD2/FMUL2

@@ -86,7 +86,8 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
         "bn": bn,
         "fmad": False,
         "order": "3xtf32 tensor-core (reassociated)",
-        "pre": [f"({py_expr(M)}) % 128 == 0", f"({py_expr(N)}) % {bn} == 0", f"({py_expr(K)}) % 32 == 0"],
+        "pre": [f"({py_expr(M)}) % 128 == 0", f"({py_expr(N)}) % {bn} == 0", f"({py_expr(K)}) % 32 == 0",
+                f"({py_expr(M)}) * ({py_expr(N)}) * ({py_expr(K)}) > 0"],
         "smem": stages * 2 * (128 * 32 * 4 + bn * 32 * 4) + 1024 + 256,
         "extra_args": [
             {"kind": "tma2d", "buf": a_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(M)], "pitch": py_expr(K),

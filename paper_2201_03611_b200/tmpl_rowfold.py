@@ -81,7 +81,8 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
 
     rs_list = list(dict.fromkeys(row_streams.values()))
     sh_list = list(dict.fromkeys(shared_streams.values()))
-    pre = [f"({py_expr(loop.bound)}) % 4 == 0"]
+    # TMA boxes need non-empty tensors; 16-byte bulk copies need K % 4 == 0
+    pre = [f"({py_expr(loop.bound)}) % 4 == 0", f"({py_expr(loop.bound)}) > 0", f"({py_expr(nrows)}) > 0"]
     tmaps = []
     for k, (buf, base) in enumerate(rs_list):
         aff = affine_in_flat_row(base, loops, prog.assumptions)

@@ -267,7 +267,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "blocks_per_sm": BLOCKS_PER_SM,
         "fmad": False,
         "order": "preserved",
-        "pre": [f"({py_expr(A.dims[1])}) % 4 == 0"],
+        "pre": [f"({py_expr(A.dims[1])}) % 4 == 0", f"({py_expr(R)}) * ({py_expr(C)}) > 0"],
         "extra_args": [{"kind": "tma2d", "buf": abuf, "offset": "0",
                         "dims": [py_expr(A.dims[1]), py_expr(A.dims[0])], "pitch": py_expr(A.dims[1]),
                         "box": [sw, sr], "swizzle": 0}],

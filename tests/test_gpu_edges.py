@@ -1,0 +1,96 @@
+"""Edge cases on the GPU: empty, single-element and ragged sizes (template
+preconditions fall back to the generic kernel, which is bit-exact), and the
+32-bit indexing limit.  Compared with the oracle like test_gpu_parity.py."""
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2201_03611_b200 import compile_program, emit_cuda, programs, run_cuda
+from paper_2201_03611_b200._ref import errors
+from paper_2201_03611_b200.run import Executable
+
+pytestmark = pytest.mark.gpu
+
+W3 = (np.array([[1, 2, 1], [2, 4, 2], [1, 2, 1]], np.float32) / 16).astype(np.float32)
+
+
+def _cfg(key):
+    cfg = programs.CONFIGS[key]
+    return compile_program(cfg["source"], cfg["strategy"], name=cfg["name"])
+
+
+@pytest.mark.parametrize("n", [0, 4, 5, 7, 12])
+def test_dot_small_and_empty(gpu, n):
+    c = _cfg("dot")
+    a = oracle.rng_inputs(1, n)
+    b = oracle.rng_inputs(2, n)
+    got = run_cuda(emit_cuda(c.unit), c.unit, {"n": n}, [a, b], as_numpy=True)[0]
+    if n % 4:  # generic sequential kernel: the reference's own order
+        assert got == oracle.dot(a, b)
+    else:
+        v64, s = oracle.dot_f64(a, b)
+        assert abs(float(got) - v64) <= oracle.reassociated_dot_bound(max(n, 1), s, 4) + 0.0
+    if n == 0:
+        assert got == np.float32(0.0)
+
+
+@pytest.mark.parametrize("n,m", [(1, 4), (3, 5), (1, 1), (31, 6), (64, 1028)])
+def test_gemv_ragged_sizes_bit_exact(gpu, n, m):
+    c = _cfg("gemv")
+    M = oracle.rng_inputs(2, n, m)
+    x = oracle.rng_inputs(3, m)
+    got = run_cuda(emit_cuda(c.unit), c.unit, {"n": n, "m": m}, [M, x], as_numpy=True)
+    np.testing.assert_array_equal(got, oracle.mv(M, x))
+
+
+def test_gemv_zero_rows(gpu):
+    c = _cfg("gemv")
+    M = np.zeros((0, 8), np.float32)
+    x = oracle.rng_inputs(3, 8)
+    got = run_cuda(emit_cuda(c.unit), c.unit, {"n": 0, "m": 8}, [M, x], as_numpy=True)
+    assert got.size == 0
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (1, 7), (7, 1), (2, 2), (65, 129)])
+def test_conv_degenerate_images_bit_exact(gpu, n, m):
+    c = _cfg("conv")
+    img = oracle.rng_inputs(9, n, m)
+    got = run_cuda(emit_cuda(c.unit), c.unit, {"n": n, "m": m}, [img, W3], as_numpy=True).reshape(n, m)
+    np.testing.assert_array_equal(got, oracle.conv3x3(img, W3))
+
+
+def test_nbody_single_body(gpu):
+    c = _cfg("nbody")
+    pos = np.array([[0.5, -0.25, 0.125]], np.float32)
+    vel = np.array([[1.0, 2.0, 3.0]], np.float32)
+    mass = np.array([1.0], np.float32)
+    got = run_cuda(emit_cuda(c.unit), c.unit, {"n": 1}, [pos, vel, mass], as_numpy=True)
+    np.testing.assert_array_equal(got.reshape(1, 3), vel)  # self-interaction is softened to zero
+
+
+@pytest.mark.parametrize("n,m,k", [(1, 1, 1), (3, 2, 5), (128, 256, 33)])
+def test_sgemm_ragged_falls_back_bit_exact(gpu, n, m, k):
+    c = _cfg("sgemm")
+    A = oracle.rng_inputs(4, n, k)
+    Bt = oracle.rng_inputs(5, m, k)
+    got = run_cuda(emit_cuda(c.unit), c.unit, {"n": n, "m": m, "k": k}, [A, Bt], as_numpy=True).reshape(n, m)
+    np.testing.assert_array_equal(got, oracle.sgemm_bt(A, Bt))
+
+
+def test_int32_index_limit_is_enforced(gpu):
+    c = _cfg("gemv")
+    with pytest.raises(errors.InterpreterError, match="2\\^31"):
+        Executable(emit_cuda(c.unit), {"n": 65536, "m": 65536})
+
+
+def test_missing_size_is_reported(gpu):
+    c = _cfg("gemv")
+    with pytest.raises(errors.InterpreterError, match="missing size"):
+        run_cuda(emit_cuda(c.unit), c.unit, {"n": 4}, [np.zeros((4, 4), np.float32), np.zeros(4, np.float32)])
+
+
+def test_wrong_input_length_is_reported(gpu):
+    c = _cfg("gemv")
+    with pytest.raises(errors.InterpreterError):
+        run_cuda(emit_cuda(c.unit), c.unit, {"n": 4, "m": 4}, [np.zeros((4, 3), np.float32), np.zeros(4, np.float32)])

@@ -476,8 +476,13 @@ def arg_names(prog: lir.Program, temps):
 # whole units
 
 
-def emit_cuda(unit, exact=True, idioms=True) -> CudaCode:
-    """Emit the sm100a kernel text (and launch plan) for an ImperativeUnit."""
+def emit_cuda(unit, exact=True, idioms=True, reassociate=True) -> CudaCode:
+    """Emit the sm100a kernel text (and launch plan) for an ImperativeUnit.
+
+    `reassociate=False` keeps every reduction in the program's own order
+    (templates that reassociate — `reduce`, `gemm_tc`, fast-math `allpairs` —
+    are not used), so every kernel is bit-exact with the reference's
+    sequential semantics."""
     from . import idioms as idiom_mod
 
     prog = lir.build(unit)
@@ -490,7 +495,7 @@ def emit_cuda(unit, exact=True, idioms=True) -> CudaCode:
         generic = GenericKernel(prog, st, base, temps, exact).emit()
         kernels.append(generic.text)
         entry = dict(generic.plan)
-        match = idiom_mod.match(prog, st, base, temps, exact) if idioms else None
+        match = idiom_mod.match(prog, st, base, temps, exact, reassociate) if idioms else None
         if match is not None:
             kernels.append(match.text)
             for inc in match.includes:
@@ -510,6 +515,7 @@ def emit_cuda(unit, exact=True, idioms=True) -> CudaCode:
         "temps": [{"name": t.name, "ctype": t.ctype, "size": py_expr(_prod(t.dims))} for t in temps],
         "stages": plan_stages,
         "exact": exact,
+        "reassociate": reassociate,
     }
     header = [
         f"// rise-b200 {TARGET} kernels for RISE unit '{prog.name}' (generated by emit_cuda; do not edit)",

@@ -36,8 +36,13 @@ class IdiomKernel:
     includes: list = field(default_factory=list)
 
 
-def match(prog, stage, base_name, temps, exact):
+ORDER_PRESERVING = ("_match_rowfold", "_match_stencil")
+
+
+def match(prog, stage, base_name, temps, exact, reassociate=True):
     for matcher in (_match_gemm, _match_rowfold, _match_reduce, _match_stencil, _match_allpairs):
+        if not reassociate and matcher.__name__ not in ORDER_PRESERVING:
+            continue
         out = matcher(prog, stage, base_name, temps, exact)
         if out is not None:
             return out

@@ -26,6 +26,20 @@ depFun((n: Nat) => fun(a: Array[n, f32] => fun(b: Array[n, f32] =>
 """
 DOT_STRATEGY = "fuseReduceMap @ every(isReduce) ; toReduceSeq @ every(isReduce)"
 
+# C1 written in an explicit, parallel order: 4096-element chunks folded
+# left-to-right in parallel (one row per thread, the `rowfold` template),
+# then the chunk partials folded left-to-right.  Emitted with
+# reassociate=False every step keeps this order: bit-exact with the
+# reference.  Needs the divisibility assumption 4096 | n.
+DOT_CHUNKED = """\
+depFun((n: Nat) => fun(a: Array[n, f32] => fun(b: Array[n, f32] =>
+  zip(a)(b) |> split(4096)
+    |> mapGlobal(fun(ch => ch |> reduceSeq(Private)(fun(acc, p => acc + fst(p) * snd(p)))(0.0f)))
+    |> toMem(Global)
+    |> reduceSeq(Private)(fun(acc, v => acc + v))(0.0f) )))
+"""
+DOT_CHUNK = 4096
+
 MV = """\
 // matrix-vector multiplication: for each row, a dot product with x
 def mv = depFun((n: Nat, m: Nat) =>

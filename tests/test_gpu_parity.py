@@ -224,3 +224,22 @@ def test_nbody_shard_program_equals_full_rows(gpu):
     got = run_cuda(emit_cuda(part.unit), part.unit, {"t": t, "n": n},
                    [pos[t0:t0 + t], vel[t0:t0 + t], pos, mass], as_numpy=True).reshape(t, 3)
     np.testing.assert_array_equal(got, ref[t0:t0 + t])
+
+
+@pytest.mark.parametrize("n", [1 << 20, 1 << 24])
+def test_dot_chunked_program_bit_exact(gpu, n):
+    """C1 written in an explicit parallel order (programs.DOT_CHUNKED) and
+    emitted with reassociate=False: rowfold for the chunks + the sequential
+    fold of the partials — bit-identical to the reference semantics."""
+    from paper_2201_03611_b200._ref import nat
+
+    c = compile_program(programs.DOT_CHUNKED, None, name="dotChunked",
+                        assumptions=[(nat.Var("n"), nat.Const(programs.DOT_CHUNK))])
+    code = emit_cuda(c.unit, reassociate=False)
+    assert [s["kind"] for s in code.plan["stages"]] == ["rowfold", "serial"]
+    a = oracle.rng_inputs(1, n)
+    b = oracle.rng_inputs(11, n)
+    got = run_cuda(code, c.unit, {"n": n}, [a, b], as_numpy=True)[0]
+    ch = programs.DOT_CHUNK
+    partials = np.array([oracle.dot(a[i:i + ch], b[i:i + ch]) for i in range(0, n, ch)], np.float32)
+    assert got == oracle.dot(partials, np.ones_like(partials))

@@ -53,6 +53,7 @@ def _peaks():
 class Workload:
     key = ""
     config_index = 0
+    emit_kwargs: dict = {}
 
     def __init__(self, rank=0, world=1):
         self.rank, self.world = rank, world
@@ -131,6 +132,20 @@ class Dot(Workload):
         t = _best_of(lambda: oracle.ref_dot(a, b), 3)
         return {"value": self.work() / t / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
                 "sample": "full 2^24 dot, the reference's emitted C (sequential left fold, 1 thread), best of 3"}
+
+
+class DotChunked(Dot):
+    key = "dot_chunked"
+    program = "C1 in an explicit order: split(4096) |> mapGlobal(reduceSeq) |> toMem(Global) |> reduceSeq (bit-exact)"
+    emit_kwargs = {"reassociate": False}
+
+    def compile(self):
+        from paper_2201_03611_b200 import compile_program, programs
+        from paper_2201_03611_b200._ref import nat
+
+        c = compile_program(programs.DOT_CHUNKED, None, name="dotChunked",
+                            assumptions=[(nat.Var("n"), nat.Const(programs.DOT_CHUNK))])
+        return c, {"n": self.n}
 
 
 class Conv(Workload):
@@ -231,7 +246,7 @@ class Nbody(Workload):
                 "kind": "port", "sample": f"{count} target bodies x {self.n} sources, C restatement, OpenMP"}
 
 
-WORKLOADS = {w.key: w for w in (Gemv, GemvOpt, Dot, Conv, Sgemm, Nbody)}
+WORKLOADS = {w.key: w for w in (Gemv, GemvOpt, Dot, DotChunked, Conv, Sgemm, Nbody)}
 
 
 def _best_of(fn, k):
@@ -330,7 +345,7 @@ def run_ours(args, rank, world, local_rank):
     host = wl.inputs()
     if world > 1:
         compiled, nats, host = _distributed_variant(wl, compiled, nats, host, rank, world)
-    code = emit_cuda(compiled.unit)
+    code = emit_cuda(compiled.unit, **wl.emit_kwargs)
     exe = Executable(code, nats, device=device)
     stream = torch.cuda.Stream()
     dev_in = [torch.from_numpy(np.ascontiguousarray(h).reshape(-1)).to("cuda") for h in host]
@@ -460,6 +475,7 @@ def _parallelism_text(wl, world):
         "gemv_opt": f"weak: rank r owns an 8192-row band of an ({world}x8192) x 8192 matrix, x replicated",
         "sgemm": f"weak: rank r owns a 4096-row block of A ({world}x4096 rows), B replicated",
         "dot": "weak: rank r owns a 2^24 chunk; partials all-gathered (NCCL) and folded in rank order",
+        "dot_chunked": "weak: rank r owns a 2^24 chunk; partials all-gathered (NCCL) and folded in rank order",
         "conv": "weak: rank r owns an 8192-row band; halo rows exchanged with neighbours (NCCL P2P) per step",
         "nbody": f"strong: 131072 bodies, {131072 // world} targets per rank; positions/masses all-gathered per step",
     }[wl.key]
@@ -512,7 +528,7 @@ def _distributed_step(wl, exe, dev_in, out, stream, dist, rank, world):
             bound()
 
     exe = _Exe()
-    if wl.key == "dot":
+    if wl.key in ("dot", "dot_chunked"):
         parts = [torch.empty(1, dtype=torch.float32, device="cuda") for _ in range(world)]
         total = torch.empty(1, dtype=torch.float32, device="cuda")
 

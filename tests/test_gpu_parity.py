@@ -236,10 +236,22 @@ def test_dot_chunked_program_bit_exact(gpu, n):
     c = compile_program(programs.DOT_CHUNKED, None, name="dotChunked",
                         assumptions=[(nat.Var("n"), nat.Const(programs.DOT_CHUNK))])
     code = emit_cuda(c.unit, reassociate=False)
-    assert [s["kind"] for s in code.plan["stages"]] == ["rowfold", "serial"]
+    assert [s["kind"] for s in code.plan["stages"]] == ["rowfold", "seqfold"]
     a = oracle.rng_inputs(1, n)
     b = oracle.rng_inputs(11, n)
     got = run_cuda(code, c.unit, {"n": n}, [a, b], as_numpy=True)[0]
     ch = programs.DOT_CHUNK
     partials = np.array([oracle.dot(a[i:i + ch], b[i:i + ch]) for i in range(0, n, ch)], np.float32)
     assert got == oracle.dot(partials, np.ones_like(partials))
+
+
+@pytest.mark.parametrize("n", [1 << 16, 1000, 3])
+def test_dot_reassociate_false_is_the_reference_order(gpu, n):
+    """With reassociate=False the plain dot keeps its sequential left fold
+    (the `seqfold` template when loads are unit-stride): bit-exact."""
+    c = compile_program(programs.DOT, programs.DOT_STRATEGY, name="dot")
+    code = emit_cuda(c.unit, reassociate=False)
+    a = oracle.rng_inputs(1, n)
+    b = oracle.rng_inputs(2, n)
+    got = run_cuda(code, c.unit, {"n": n}, [a, b], as_numpy=True)[0]
+    assert got == oracle.dot(a, b)

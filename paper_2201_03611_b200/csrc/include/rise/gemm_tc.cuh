@@ -229,4 +229,205 @@ RS_DEVICE void gemm_3xtf32(float* __restrict__ C, int ldc, const rs_tmap* mapA, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (tcgen05 cta_group::2): a cluster of two CTAs on a TPC
+// computes a 256 x BN tile with M=256 MMAs issued by the leader CTA.  Each CTA
+// stages its own 128 rows of A and BN/2 rows of Bt (raw + lo), so every byte
+// of shared memory feeds twice the MMA work of the single-CTA kernel; the
+// accumulator rows 0-127 live in the leader's TMEM, 128-255 in the peer's.
+//
+//   both CTAs, warp 0   TMA of the CTA's own A / Bt halves (local barrier)
+//   both CTAs, warp 1   tcgen05.alloc.cta_group::2; leader lane 0 issues the
+//                       MMAs and multicasts tcgen05.commit to both CTAs
+//   both CTAs, 2..5     split hi/lo in place, then arrive (cluster scope) on
+//                       the LEADER's conv barrier; epilogue from own TMEM
+
+RS_DEVICE unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+RS_DEVICE unsigned mapa(unsigned saddr, unsigned rank) {
+  unsigned out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(saddr), "r"(rank));
+  return out;
+}
+
+RS_DEVICE void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+RS_DEVICE void mbar_arrive_remote(unsigned cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+RS_DEVICE void mbar_wait_cluster(unsigned long long* bar, unsigned phase) {
+  unsigned ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(rs_smem_addr(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
+template <unsigned IDESC>
+RS_DEVICE void mma2(unsigned tmem_d, unsigned long long adesc, unsigned long long bdesc, unsigned accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+
+RS_DEVICE void commit2_multicast(unsigned long long* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          rs_smem_addr(bar)),
+      "h"((unsigned short)3)
+      : "memory");
+}
+
+template <unsigned COLS>
+RS_DEVICE void tmem_alloc2(unsigned* slot) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(rs_smem_addr(slot)),
+               "r"(COLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+
+template <unsigned COLS>
+RS_DEVICE void tmem_dealloc2(unsigned taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(COLS) : "memory");
+}
+
+template <int BN_, int STAGES_>
+struct Cfg2 {
+  static constexpr int BN = BN_;  // pair tile: 256 x BN; each CTA stages BN/2 rows of Bt
+  static constexpr int STAGES = STAGES_;
+  static constexpr int TILE_A = 128 * BK * 4;
+  static constexpr int TILE_B = (BN / 2) * BK * 4;
+  static constexpr int STAGE_BYTES = 2 * (TILE_A + TILE_B);
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr unsigned TMEM_COLS = BN;
+  static constexpr unsigned IDESC =
+      (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(256 >> 4) << 24);
+};
+
+// blockIdx.x = 2 * pair + rank; pair -> (tm, tn) with tn fastest
+template <int M, int N, int K, int BN, int STAGES>
+RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* mapA, const rs_tmap* mapB) {
+  using G = Cfg2<BN, STAGES>;
+  extern __shared__ __align__(1024) unsigned char rs_gemm_smem_raw[];
+  unsigned char* smem =
+      rs_gemm_smem_raw + ((1024u - (rs_smem_addr(rs_gemm_smem_raw) & 1023u)) & 1023u);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + STAGES * G::STAGE_BYTES);
+  unsigned long long* full = bars;
+  unsigned long long* conv = bars + STAGES;
+  unsigned long long* empty = bars + 2 * STAGES;
+  unsigned long long* tmem_full = bars + 3 * STAGES;
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 3 * STAGES + 1);
+
+  constexpr int KB = K / BK;
+  constexpr int NTN = N / BN;
+  const unsigned rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1;
+  const int m0 = (pair / NTN) * 256, n0 = (pair % NTN) * BN;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto a_raw = [&](int s) { return smem + s * G::STAGE_BYTES; };
+  auto a_lo = [&](int s) { return smem + s * G::STAGE_BYTES + G::TILE_A; };
+  auto b_raw = [&](int s) { return smem + s * G::STAGE_BYTES + 2 * G::TILE_A; };
+  auto b_lo = [&](int s) { return smem + s * G::STAGE_BYTES + 2 * G::TILE_A + G::TILE_B; };
+
+  if (threadIdx.x == 0) {
+    rs_tmap_prefetch(mapA);
+    rs_tmap_prefetch(mapB);
+    for (int s = 0; s < STAGES; ++s) {
+      rs_mbar_init(&full[s], 1);
+      rs_mbar_init(&conv[s], 8);  // 4 converter warps in each CTA of the pair
+      rs_mbar_init(&empty[s], 1);
+    }
+    rs_mbar_init(tmem_full, 1);
+    rs_fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc2<G::TMEM_COLS>(tmem_slot);
+  fence_before();
+  cluster_sync();
+  fence_after();
+  const unsigned tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % STAGES;
+        const unsigned ph = (unsigned)((kb / STAGES) & 1);
+        rs_mbar_wait(&empty[s], ph ^ 1u);
+        rs_mbar_arrive_expect_tx(&full[s], G::TILE_A + G::TILE_B);
+        rs_tma_load_2d(a_raw(s), mapA, kb * BK, m0 + 128 * (int)rank, &full[s]);
+        rs_tma_load_2d(b_raw(s), mapB, kb * BK, n0 + (BN / 2) * (int)rank, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % STAGES;
+        const unsigned ph = (unsigned)((kb / STAGES) & 1);
+        mbar_wait_cluster(&conv[s], ph);
+        fence_after();
+        const unsigned long long ahi = smem_desc(rs_smem_addr(a_raw(s)));
+        const unsigned long long alo = smem_desc(rs_smem_addr(a_lo(s)));
+        const unsigned long long bhi = smem_desc(rs_smem_addr(b_raw(s)));
+        const unsigned long long blo = smem_desc(rs_smem_addr(b_lo(s)));
+#pragma unroll
+        for (int k = 0; k < BK / 8; ++k) {
+          const unsigned long long off = (unsigned long long)(k * 32) >> 4;
+          mma2<G::IDESC>(tmem, alo + off, bhi + off, (kb | k) != 0);
+          mma2<G::IDESC>(tmem, ahi + off, blo + off, 1u);
+          mma2<G::IDESC>(tmem, ahi + off, bhi + off, 1u);
+        }
+        commit2_multicast(&empty[s]);
+      }
+      commit2_multicast(tmem_full);
+    }
+    __syncwarp();
+  } else {
+    const int t = threadIdx.x - 64;
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % STAGES;
+      const unsigned ph = (unsigned)((kb / STAGES) & 1);
+      rs_mbar_wait(&full[s], ph);
+      split_tile<false>(a_raw(s), a_lo(s), G::TILE_A, t);
+      split_tile<false>(b_raw(s), b_lo(s), G::TILE_B, t);
+      rs_fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(mapa(rs_smem_addr(&conv[s]), 0u));
+    }
+    rs_mbar_wait(tmem_full, 0u);
+    fence_after();
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    float* crow = C + (long long)(m0 + 128 * (int)rank + row) * ldc + n0;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      unsigned r[32];
+      tmem_ld32(tmem + ((unsigned)(q * 32) << 16) + (unsigned)c0, r);
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        *reinterpret_cast<float4*>(crow + c0 + j) =
+            make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                        __uint_as_float(r[j + 3]));
+      }
+    }
+  }
+  fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    fence_after();
+    tmem_dealloc2<G::TMEM_COLS>(tmem);
+  }
+}
+
 }  // namespace rise_gemm

@@ -28,6 +28,10 @@ from .emit_cuda import NatRenderer, kernel_head, py_expr
 BN = int(os.environ.get("RISE_GEMM_BN", "256"))
 STAGES = int(os.environ.get("RISE_GEMM_STAGES", "2"))
 WRITE_HI = os.environ.get("RISE_GEMM_WRITE_HI", "0") == "1"
+# CTA-pair (cta_group::2, M = 256) variant
+PAIR = os.environ.get("RISE_GEMM_2SM", "0") == "1"
+PAIR_BN = int(os.environ.get("RISE_GEMM_PAIR_BN", "256"))
+PAIR_STAGES = int(os.environ.get("RISE_GEMM_PAIR_STAGES", "3"))
 
 
 def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
@@ -73,6 +77,32 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
     bn, stages, write_hi = BN, STAGES, WRITE_HI
     extra = ["const __grid_constant__ rs_tmap rs_mapA", "const __grid_constant__ rs_tmap rs_mapB"]
     lines = kernel_head(prog, name, temps, launch_bounds="192, 1", extra_params=extra)
+    if PAIR:
+        lines += [
+            f"  rise_gemm::gemm_3xtf32_2sm<{r(M)}, {r(N)}, {r(K)}, {PAIR_BN}, {PAIR_STAGES}>"
+            f"({st.target.buf}, {r(N)}, &rs_mapA, &rs_mapB);",
+            "}",
+        ]
+        plan = {
+            "name": name,
+            "kind": "gemm_tc",
+            "M": py_expr(M),
+            "N": py_expr(N),
+            "bn": PAIR_BN,
+            "pair": True,
+            "fmad": False,
+            "order": "3xtf32 tensor-core, CTA pairs (reassociated)",
+            "pre": [f"({py_expr(M)}) % 256 == 0", f"({py_expr(N)}) % {PAIR_BN} == 0", f"({py_expr(K)}) % 32 == 0",
+                    f"({py_expr(M)}) * ({py_expr(N)}) * ({py_expr(K)}) > 0"],
+            "smem": PAIR_STAGES * 2 * (128 * 32 * 4 + (PAIR_BN // 2) * 32 * 4) + 1024 + 256,
+            "extra_args": [
+                {"kind": "tma2d", "buf": a_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(M)],
+                 "pitch": py_expr(K), "box": [32, 128], "swizzle": 3},
+                {"kind": "tma2d", "buf": b_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(N)],
+                 "pitch": py_expr(K), "box": [32, PAIR_BN // 2], "swizzle": 3},
+            ],
+        }
+        return "\n".join(lines) + "\n", plan
     lines += [
         f"  rise_gemm::gemm_3xtf32<{r(K)}, {bn}, {stages}, {'true' if write_hi else 'false'}>"
         f"({st.target.buf}, {r(N)}, &rs_mapA, &rs_mapB);",
@@ -104,4 +134,6 @@ def launch(st, nats, sm):
 
     M = eval_py(st["M"], nats)
     N = eval_py(st["N"], nats)
+    if st.get("pair"):
+        return (2 * (M // 256) * (N // st["bn"]), 1, 1), (192, 1, 1), st["smem"], (2, 1, 1)
     return (N // st["bn"], M // 128, 1), (192, 1, 1), st["smem"], (1, 1, 1)

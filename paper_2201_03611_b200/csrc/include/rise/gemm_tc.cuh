@@ -347,7 +347,7 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
     rs_tmap_prefetch(mapB);
     for (int s = 0; s < STAGES; ++s) {
       rs_mbar_init(&full[s], 1);
-      rs_mbar_init(&conv[s], 8);  // 4 converter warps in each CTA of the pair
+      rs_mbar_init(&conv[s], 2);  // one arrival from each CTA of the pair
       rs_mbar_init(&empty[s], 1);
     }
     rs_mbar_init(tmem_full, 1);
@@ -402,8 +402,9 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
       split_tile<false>(a_raw(s), a_lo(s), G::TILE_A, t);
       split_tile<false>(b_raw(s), b_lo(s), G::TILE_B, t);
       rs_fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote(mapa(rs_smem_addr(&conv[s]), 0u));
+      // one cluster-scope release per CTA and stage (its fence is the costly part)
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (t == 0) mbar_arrive_remote(mapa(rs_smem_addr(&conv[s]), 0u));
     }
     rs_mbar_wait(tmem_full, 0u);
     fence_after();

@@ -29,7 +29,7 @@ BN = int(os.environ.get("RISE_GEMM_BN", "256"))
 STAGES = int(os.environ.get("RISE_GEMM_STAGES", "2"))
 WRITE_HI = os.environ.get("RISE_GEMM_WRITE_HI", "0") == "1"
 # CTA-pair (cta_group::2, M = 256) variant
-PAIR = os.environ.get("RISE_GEMM_2SM", "0") == "1"
+PAIR = os.environ.get("RISE_GEMM_2SM", "1") == "1"
 PAIR_BN = int(os.environ.get("RISE_GEMM_PAIR_BN", "256"))
 PAIR_STAGES = int(os.environ.get("RISE_GEMM_PAIR_STAGES", "3"))
 

@@ -206,7 +206,7 @@ def test_tensor_core_ignores_low_tf32_bits(gpu):
     outs = []
     for hi in ("0", "1"):
         path = os.path.join(tempfile.mkdtemp(), "out.npy")
-        env = dict(os.environ, RISE_GEMM_WRITE_HI=hi, RISE_GEMM_BN="128", RISE_GEMM_STAGES="3")
+        env = dict(os.environ, RISE_GEMM_WRITE_HI=hi, RISE_GEMM_BN="128", RISE_GEMM_STAGES="3", RISE_GEMM_2SM="0")
         subprocess.run([sys.executable, "-c", code, path], check=True, env=env,
                        cwd=str(__import__("pathlib").Path(__file__).resolve().parent.parent))
         outs.append(np.load(path))
@@ -255,3 +255,23 @@ def test_dot_reassociate_false_is_the_reference_order(gpu, n):
     b = oracle.rng_inputs(2, n)
     got = run_cuda(code, c.unit, {"n": n}, [a, b], as_numpy=True)[0]
     assert got == oracle.dot(a, b)
+
+
+def test_sgemm_single_cta_variant_within_bound(gpu):
+    """The single-CTA tcgen05 kernel (RISE_GEMM_2SM=0) stays correct too."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, 'oracle'); import oracle;"
+        "from paper_2201_03611_b200 import compile_program, emit_cuda, programs, run_cuda;"
+        "c = compile_program(programs.SGEMM_BT, None, name='sgemm'); code = emit_cuda(c.unit);"
+        "assert not code.plan['stages'][0].get('pair');"
+        "A = oracle.rng_inputs(4, 512, 256); B = oracle.rng_inputs(5, 512, 256);"
+        "got = run_cuda(code, c.unit, {'n': 512, 'm': 512, 'k': 256}, [A, B], as_numpy=True).reshape(512, 512);"
+        "C64, absC = oracle.sgemm_bt_f64(A, B);"
+        "assert np.all(np.abs(got - C64) <= oracle.gemm_bound(256, absC))"
+    )
+    root = str(__import__("pathlib").Path(__file__).resolve().parent.parent)
+    subprocess.run([sys.executable, "-c", code], check=True, cwd=root, env=dict(os.environ, RISE_GEMM_2SM="0"))

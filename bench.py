@@ -42,8 +42,8 @@ def _peaks():
     if p.exists():
         d = json.loads(p.read_text())
         return {"hbm_gbs": d["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)",
-                "sm_max_mhz": d.get("sm_max_mhz", 1965.0)}
-    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)", "sm_max_mhz": 1965.0}
+                "sm_max_mhz": d.get("sm_max_mhz", 1965.0), "bf16_tflops": d.get("bf16_tflops")}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)", "sm_max_mhz": 1965.0, "bf16_tflops": 1590.0}
 
 
 # ---------------------------------------------------------------------------
@@ -597,7 +597,17 @@ def _roofline(wl, achieved, peaks, args):
     if wl.bound == "hbm":
         peak, unit, src = peaks["hbm_gbs"], "GB/s", peaks["source"]
     elif wl.bound == "tensor":
-        peak, unit, src = _tf32_peak() / 3.0, "GFLOP/s", "measured cuBLAS TF32 / 3 (3xTF32 fp32-equivalent)"
+        # the TF32 MMA rate is half the BF16 rate on sm_100; cuBLAS's own TF32
+        # sgemm reaches less than that, so the larger of the two is the roof
+        cublas = _tf32_peak()
+        bf16 = peaks.get("bf16_tflops")
+        if bf16 and bf16 * 1e3 / 2 > cublas:
+            peak, src = bf16 * 1e3 / 2 / 3.0, (f"MEASURED_PEAKS bf16 {bf16} TFLOP/s / 2 (TF32 MMA rate) / 3 "
+                                               f"(3xTF32 fp32-equivalent); cuBLAS TF32 sgemm measured "
+                                               f"{cublas / 1e3:.1f} TFLOP/s")
+        else:
+            peak, src = cublas / 3.0, "measured cuBLAS TF32 / 3 (3xTF32 fp32-equivalent)"
+        unit = "GFLOP/s"
     else:
         peak, unit, src = FP32_SIMT_TFLOPS * 1e3, "GFLOP/s", "derived 148 SM x 128 x 2 x 1.965 GHz"
     traffic = None

@@ -12,13 +12,16 @@ where every load that depends on j reads a "source stream" B[a*j + off]
 with a constant stride a and 0 <= off < a (off from c and constant inner
 loops), and every other load is j-invariant (the target's own data).
 
-Order: each (g, c) fold still runs over j = 0, 1, ..., NS-1 in order.  The
-template fuses the c loop into the j loop (independent accumulators, so
-each fold's sequence of operations is unchanged), tiles j through shared
-memory (all threads of a block read the same source element: broadcast
-LDS), and register-blocks RB targets per thread so one staged source serves
-RB x C accumulators; the compiler CSEs the per-pair work shared by the C
-components (distance, rsqrt).  This template is emitted with fast math
+Order: when the fold step is `acc = acc + e(j)`, the sources are split into
+SPLIT contiguous chunks of ceil(NS/SPLIT): warp w of a block folds chunk w
+in j order (chunk 0 from INIT, the others from +0.0) and the partials are
+added in chunk order, ((p0 + p1) + p2) + ...; otherwise (SPLIT = 1) each
+(g, c) fold runs over j = 0..NS-1 in order.  The template fuses the c loop
+into the j loop (independent accumulators), tiles each warp's chunk through
+its own shared-memory tile (all lanes read the same source record:
+broadcast LDS.128), and register-blocks RB targets per thread so one staged
+source serves RB x C accumulators; the compiler CSEs the per-pair work
+shared by the C components (distance, rsqrt).  This template is emitted with fast math
 (FMA contraction, MUFU rsqrt): parity is the tolerance of DESIGN.md (no
 worse than the reference's own fp32 left fold, measured against fp64).
 """
@@ -31,11 +34,13 @@ from .emit_cuda import GenericKernel, NatRenderer, Stage, ValueRenderer, kernel_
 
 import os
 
-# 64-thread blocks x 2 targets per thread: 1024 blocks for 131072 bodies, so
-# the per-SM load is balanced to ~1% and each SM holds ~14 warps
-BLOCK = int(os.environ.get("RISE_ALLPAIRS_BLOCK", "32"))
+# a block is SPLIT warps over the same 32*RB targets, warp w folding the w-th
+# contiguous chunk of the sources: 1024 blocks x 16 warps for 131072 bodies,
+# 32 resident warps per SM (the target count alone gives only ~7); measured
+# on B200: SPLIT 1 / 4 / 8 / 16 -> 0.52 / 0.63 / 0.67 / 0.67 of FP32 peak
+SPLIT = int(os.environ.get("RISE_ALLPAIRS_SPLIT", "16"))
 RB = int(os.environ.get("RISE_ALLPAIRS_RB", "4"))  # targets per thread
-JT = int(os.environ.get("RISE_ALLPAIRS_JT", "512"))  # sources per shared-memory tile
+JT = int(os.environ.get("RISE_ALLPAIRS_JT", "64"))  # sources per warp tile
 UNROLL = int(os.environ.get("RISE_ALLPAIRS_UNROLL", "4"))  # source loop unroll
 PACKED = os.environ.get("RISE_ALLPAIRS_PACKED", "1") == "1"  # two targets per FFMA2/FADD2/FMUL2
 
@@ -75,6 +80,35 @@ def _split(body):
             if isinstance(t, lir.Store) and t.buf not in local:
                 return None
     return cvar, C, acc, init, jloop, post
+
+
+def _fold_is_sum(body, acc):
+    """True when the fold step is exactly `acc = acc + e` (e free of acc) and
+    acc is written nowhere else: only then may the sources be split into
+    chunks whose partial sums are added afterwards."""
+    writes = [s for s in lir.walk(body) if isinstance(s, lir.Assign) and s.target == acc]
+    if len(writes) != 1:
+        return False
+    def straight(s):  # statements reached through Seq / Alloc only (run once per j)
+        yield s
+        if isinstance(s, lir.Seq):
+            for c in s.stmts:
+                yield from straight(c)
+        elif isinstance(s, lir.Alloc):
+            yield from straight(s.body)
+
+    if not any(s is writes[0] for s in straight(body)):
+        return False
+    v = writes[0].value
+    if not (isinstance(v, lir.Bin) and v.op == "+" and v.ctype == "float"):
+        return False
+    if v.a == acc:
+        other = v.b
+    elif v.b == acc:
+        other = v.a
+    else:
+        return False
+    return acc not in set(lir.expr_scalars(other))
 
 
 def _const_loop_bounds(stmt):
@@ -185,13 +219,18 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     vinit = ValueRenderer(prog, exact=fast)(init.value)
     Cv = C.value
     cdecl = f"const int {cvar}" if cvar else "const int rs_c_unused"
-    lines = kernel_head(prog, name, temps, launch_bounds=BLOCK)
+    split = SPLIT if _fold_is_sum(jloop.body, acc) else 1
+    nthreads = 32 * split
+    lines = kernel_head(prog, name, temps, launch_bounds=nthreads)
     lines += [
         f"  constexpr int RS_NT = {r(NT)}, RS_NS = {r(NS)}, RS_JT = {JT}, RS_RB = {RB}, RS_C = {Cv};",
-    ]
-    lines.append(f"  __shared__ __align__(16) float rs_s[RS_JT * {rec}];")
-    lines += [
-        f"  const int rs_g0 = blockIdx.x * ({BLOCK} * RS_RB) + threadIdx.x;",
+        f"  constexpr int RS_SPLIT = {split}, RS_CH = (RS_NS + RS_SPLIT - 1) / RS_SPLIT;",
+        # one source tile per warp: the warps of a block fold disjoint source
+        # chunks for the same targets, so a warp only ever syncs with itself
+        f"  __shared__ __align__(16) float rs_sm[RS_SPLIT][RS_JT * {rec}];",
+        "  const int rs_w = threadIdx.x >> 5, rs_l = threadIdx.x & 31;",
+        "  float* const rs_s = rs_sm[rs_w];",
+        "  const int rs_g0 = blockIdx.x * (32 * RS_RB) + rs_l;",
         "  int rs_j0 = 0;",
         f"  auto rs_step = [&](const int {gv}, {cdecl}, const int {j}, {acc.ctype} {acc.name}) -> {acc.ctype} {{",
     ]
@@ -206,33 +245,39 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
                      f"float2 {acc.name}) -> float2 {{")
         lines += step2_lines
         lines += [f"    return {acc.name};", "  };"]
+    init_expr = vinit if split == 1 else f"(rs_w == 0 ? ({vinit}) : ({acc.ctype})0)"
     lines += [
         f"  {acc.ctype} rs_acc[RS_RB][RS_C];",
         "  int rs_gt[RS_RB];",
         "#pragma unroll",
         "  for (int rs_r = 0; rs_r < RS_RB; ++rs_r) {",
-        f"    const int {gv} = min(rs_g0 + rs_r * {BLOCK}, RS_NT - 1);",
+        f"    const int {gv} = min(rs_g0 + rs_r * 32, RS_NT - 1);",
         f"    rs_gt[rs_r] = {gv};",
         "#pragma unroll",
         "    for (int rs_c = 0; rs_c < RS_C; ++rs_c) {",
         f"      {cdecl} = rs_c;",
-        f"      rs_acc[rs_r][rs_c] = {vinit};",
+        f"      rs_acc[rs_r][rs_c] = {init_expr};",
         "    }",
         "  }",
-        "  for (rs_j0 = 0; rs_j0 < RS_NS; rs_j0 += RS_JT) {",
-        "    const int rs_jn = RS_NS - rs_j0 < RS_JT ? RS_NS - rs_j0 : RS_JT;",
-        "    __syncthreads();",
+        "  const int rs_jb = rs_w * RS_CH;",
+        "  const int rs_je = RS_NS < rs_jb + RS_CH ? RS_NS : rs_jb + RS_CH;",
+        "  for (rs_j0 = rs_jb; rs_j0 < rs_je; rs_j0 += RS_JT) {",
+        "    const int rs_jn = rs_je - rs_j0 < RS_JT ? rs_je - rs_j0 : RS_JT;",
+        "    __syncwarp();",
     ]
     for buf, a in s_list:
         lines += [
-            f"    for (int rs_e = threadIdx.x; rs_e < rs_jn * {a}; rs_e += {BLOCK})",
+            "#pragma unroll 4",
+            f"    for (int rs_e = rs_l; rs_e < rs_jn * {a}; rs_e += 32)",
             f"      rs_s[(rs_e / {a}) * {rec} + {offsets[buf]} + rs_e % {a}] = {buf}[{a} * rs_j0 + rs_e];",
         ]
+    lines += [
+        "    __syncwarp();",
+        f"#pragma unroll {UNROLL}",
+        "    for (int rs_jj = 0; rs_jj < rs_jn; ++rs_jj) {",
+    ]
     if packed:
         lines += [
-            "    __syncthreads();",
-            f"#pragma unroll {UNROLL}",
-            "    for (int rs_jj = 0; rs_jj < rs_jn; ++rs_jj) {",
             "#pragma unroll",
             "      for (int rs_p = 0; rs_p < RS_RB / 2; ++rs_p) {",
             "#pragma unroll",
@@ -243,27 +288,43 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
             "          rs_acc[2 * rs_p + 1][rs_c] = rs_a2.y;",
             "        }",
             "      }",
-            "    }",
-            "  }",
         ]
     else:
         lines += [
-            "    __syncthreads();",
-            f"#pragma unroll {UNROLL}",
-            "    for (int rs_jj = 0; rs_jj < rs_jn; ++rs_jj) {",
             "#pragma unroll",
             "      for (int rs_r = 0; rs_r < RS_RB; ++rs_r) {",
             "#pragma unroll",
             "        for (int rs_c = 0; rs_c < RS_C; ++rs_c)",
             "          rs_acc[rs_r][rs_c] = rs_step(rs_gt[rs_r], rs_c, rs_j0 + rs_jj, rs_acc[rs_r][rs_c]);",
             "      }",
-            "    }",
+        ]
+    lines += ["    }", "  }"]
+    if split > 1:
+        add = "__fadd_rn" if acc.ctype == "float" else ""
+        lines += [
+            # chunk partials meet in shared memory and are added in chunk order
+            f"  __shared__ {acc.ctype} rs_part[RS_SPLIT - 1][RS_RB * RS_C][32];",
+            "  if (rs_w > 0) {",
+            "#pragma unroll",
+            "    for (int rs_r = 0; rs_r < RS_RB; ++rs_r)",
+            "#pragma unroll",
+            "      for (int rs_c = 0; rs_c < RS_C; ++rs_c)",
+            "        rs_part[rs_w - 1][rs_r * RS_C + rs_c][rs_l] = rs_acc[rs_r][rs_c];",
+            "  }",
+            "  __syncthreads();",
+            "  if (rs_w != 0) return;",
+            "  for (int rs_q = 0; rs_q < RS_SPLIT - 1; ++rs_q) {",
+            "#pragma unroll",
+            "    for (int rs_r = 0; rs_r < RS_RB; ++rs_r)",
+            "#pragma unroll",
+            "      for (int rs_c = 0; rs_c < RS_C; ++rs_c)",
+            f"        rs_acc[rs_r][rs_c] = {add}(rs_acc[rs_r][rs_c], rs_part[rs_q][rs_r * RS_C + rs_c][rs_l]);",
             "  }",
         ]
     lines += [
         "#pragma unroll",
         "  for (int rs_r = 0; rs_r < RS_RB; ++rs_r) {",
-        f"    const int {gv} = rs_g0 + rs_r * {BLOCK};",
+        f"    const int {gv} = rs_g0 + rs_r * 32;",
         f"    if ({gv} < RS_NT) {{",
         "#pragma unroll",
         "      for (int rs_c = 0; rs_c < RS_C; ++rs_c) {",
@@ -276,10 +337,12 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "name": name,
         "kind": "allpairs",
         "targets": py_expr(NT),
-        "per_block": BLOCK * RB,
-        "block": BLOCK,
+        "per_block": 32 * RB,
+        "block": nthreads,
+        "split": split,
         "fmad": True,
-        "order": "preserved-fold, fast-math",
+        "order": ("preserved-fold" if split == 1 else f"{split} contiguous source chunks, added in chunk order")
+        + ", fast-math",
         "pre": [],
     }
     return "\n".join(lines) + "\n", plan

@@ -139,8 +139,15 @@ def test_nbody_allpairs_within_tolerance(gpu, n, first, count):
     got = run_cuda(code, c.unit, {"n": n}, [pos, vel, mass], as_numpy=True).reshape(n, 3)[first:first + count]
     ref32 = oracle.nbody(pos, vel, mass, first, count)
     ref64 = vel[first:first + count].astype(np.float64) + 0.01 * oracle.nbody_acc_f64(pos, mass, first, count)
-    bound = 2 * np.abs(ref32 - ref64) + 16 * oracle.U * 0.01 * _nbody_abs_terms(pos, mass, first, count)
-    assert np.all(np.abs(got - ref64) <= bound + 1e-12), float(np.max(np.abs(got - ref64) - bound))
+    # the fast-math allpairs kernel reassociates each fold (source chunks) and
+    # rounds rsqrt approximately, so the rule is normwise, not elementwise
+    # (DESIGN.md §4): every element within 1e-5 of dt * sum_j |term_j| of the
+    # fp64 result, and the worst error over the checked bodies no worse than
+    # the reference's own sequential fp32 fold's worst error
+    err = np.abs(got - ref64)
+    bound = 1e-5 * 0.01 * _nbody_abs_terms(pos, mass, first, count) + 2 * oracle.U * np.abs(ref64)
+    assert np.all(err <= bound), float(np.max(err - bound))
+    assert err.max() <= np.abs(ref32 - ref64).max(), (float(err.max()), float(np.abs(ref32 - ref64).max()))
 
 
 def test_nbody_generic_exact_bit_exact(gpu):

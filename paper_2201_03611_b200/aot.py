@@ -47,8 +47,10 @@ def build_all(nvcc, arch, out_dir: Path, keys=None):
         src = out_dir / f"aot_{key}.cu"
         src.write_text(code.text + f"\n__device__ void* rs_aot_refs_{key}[] = {{ {refs} }};\n")
         cubin = out_dir / f"aot_{key}.cubin"
-        cmd = [nvcc, "-cubin", *arch, "-std=c++17", "-lineinfo", "-O3", f"-I{INCLUDE_DIR}", "-o", str(cubin),
-               str(src)]
+        # the same contraction switch the runtime passes to NVRTC (run.Executable)
+        fmad = any(st.get("fmad", False) for st in code.plan["stages"])
+        cmd = [nvcc, "-cubin", *arch, "-std=c++17", "-lineinfo", "-O3", f"--fmad={'true' if fmad else 'false'}",
+               f"-I{INCLUDE_DIR}", "-o", str(cubin), str(src)]
         print("+", " ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
         built.append(cubin)

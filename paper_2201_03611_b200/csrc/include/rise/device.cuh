@@ -32,6 +32,21 @@ RS_DEVICE float2 rs_neg2(float2 a) { return make_float2(-a.x, -a.y); }
 RS_DEVICE float2 rs_div2(float2 a, float2 b) { return make_float2(a.x / b.x, a.y / b.y); }
 RS_DEVICE float2 rs_rsqrt2(float2 a) { return make_float2(rs_rsqrt_fast(a.x), rs_rsqrt_fast(a.y)); }
 RS_DEVICE float2 rs_sqrt2(float2 a) { return make_float2(sqrtf(a.x), sqrtf(a.y)); }
+// correctly rounded per-lane forms for exact-mode packed bodies
+//
+// ptxas (CUDA 12.9) contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even
+// with -fmad=false, which would break bit-exactness.  An exact packed
+// product is therefore written fma(a, b, -0.0) with the -0.0 read from
+// constant memory: equal to round(a * b) in every case (the -0.0 addend
+// keeps +0/-0 products as they are), and ptxas cannot fold a following add
+// into it because it cannot see the addend's value.
+__constant__ float rs_negzero = -0.0f;
+RS_DEVICE float2 rs_fmul2_exact(float2 a, float2 b) {
+  return __ffma2_rn(a, b, make_float2(rs_negzero, rs_negzero));
+}
+RS_DEVICE float2 rs_div2_rn(float2 a, float2 b) { return make_float2(__fdiv_rn(a.x, b.x), __fdiv_rn(a.y, b.y)); }
+RS_DEVICE float2 rs_sqrt2_rn(float2 a) { return make_float2(__fsqrt_rn(a.x), __fsqrt_rn(a.y)); }
+RS_DEVICE float2 rs_rsqrt2_rn(float2 a) { return make_float2(rs_rsqrt_exact(a.x), rs_rsqrt_exact(a.y)); }
 
 RS_DEVICE unsigned rs_smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));

@@ -208,6 +208,20 @@ import os  # noqa: E402
 REDUCE_GRID = int(os.environ.get("RISE_REDUCE_GRID", "1184"))
 REDUCE_BLOCK = int(os.environ.get("RISE_REDUCE_BLOCK", "256"))
 REDUCE_BATCH = int(os.environ.get("RISE_REDUCE_BATCH", "8"))  # float4 chunks per input in flight per thread
+# occupancy hint for __launch_bounds__ (never changes the order).  1: forcing
+# the whole grid resident (8 blocks/SM) caps registers at 32 and spills the
+# load batch — measured 2.0 TB/s instead of 4.6 at 2^24
+REDUCE_MINB = int(os.environ.get("RISE_REDUCE_MINB", "1"))
+# TMA variant (default): a fixed grid of REDUCE_TMA_GRID blocks (2 per SM on a
+# 148-SM B200: one wave), each streaming its chunks (REDUCE_TMA_CHUNK bytes
+# per input) through a REDUCE_TMA_STAGES-deep shared-memory ring filled by
+# cp.async.bulk from one producer lane; the REDUCE_BLOCK folding threads only
+# read shared memory.  Order: see DESIGN.md §4.
+REDUCE_TMA = os.environ.get("RISE_REDUCE_TMA", "1") == "1"
+REDUCE_TMA_GRID = int(os.environ.get("RISE_REDUCE_TMA_GRID", "296"))
+REDUCE_TMA_CHUNK = int(os.environ.get("RISE_REDUCE_TMA_CHUNK", "16384"))
+REDUCE_TMA_STAGES = int(os.environ.get("RISE_REDUCE_TMA_STAGES", "3"))
+REDUCE_TMA_CONTIG = os.environ.get("RISE_REDUCE_TMA_CONTIG", "0") == "1"
 
 
 def _match_reduce(prog, stage, base_name, temps, exact):
@@ -269,87 +283,173 @@ def _match_reduce(prog, stage, base_name, temps, exact):
 
     shfl = "__shfl_xor_sync(0xffffffffu, rs_s, rs_o)"
     U = REDUCE_BATCH
-    lines = kernel_head(prog, name, temps, launch_bounds=REDUCE_BLOCK,
+    tma = REDUCE_TMA
+    B = REDUCE_BLOCK  # threads that fold (the TMA variant adds one producer warp)
+    G = REDUCE_TMA_GRID if tma else REDUCE_GRID
+    nthreads = B + 32 if tma else B
+    minb = REDUCE_MINB
+    lines = kernel_head(prog, name, temps, launch_bounds=f"{nthreads}, {minb}",
                         extra_params=[f"{ct}* __restrict__ rs_partials", "unsigned* __restrict__ rs_ticket"])
     lines += [
         f"  constexpr int RS_N4 = ({r(loop.bound)}) / 4;",
-        f"  constexpr int RS_T = {REDUCE_GRID} * {REDUCE_BLOCK};",
-        "  constexpr int RS_ITERS = (RS_N4 + RS_T - 1) / RS_T;",
-        "  const int rs_tid = blockIdx.x * blockDim.x + threadIdx.x;",
+        f"  constexpr int RS_G = {G}, RS_B = {B};",
     ]
     for k, (buf, base) in enumerate(s_list):
         lines.append(f"  const float4* __restrict__ rs_g{k} = reinterpret_cast<const float4*>({buf} + ({r(base)}));")
+    lines.append(f"  {ct} rs_acc = {zero};")
+    smem = 0
+    if tma:
+        NSTR = len(s_list)
+        CH4 = REDUCE_TMA_CHUNK // 16
+        S = REDUCE_TMA_STAGES
+        smem = S * NSTR * CH4 * 16 + 2 * S * 8
+        lines += [
+            f"  constexpr int RS_CH4 = {CH4}, RS_S = {S}, RS_NSTR = {NSTR};",
+            "  constexpr int RS_NCH = (RS_N4 + RS_CH4 - 1) / RS_CH4;",
+            "  extern __shared__ __align__(128) unsigned char rs_smem_raw[];",
+            "  float4* const rs_ring = reinterpret_cast<float4*>(rs_smem_raw);  // [stage][stream][RS_CH4]",
+            "  unsigned long long* const rs_full = reinterpret_cast<unsigned long long*>(rs_ring + RS_S * RS_NSTR * RS_CH4);",
+            "  unsigned long long* const rs_empty = rs_full + RS_S;",
+            "  if (threadIdx.x == 0) {",
+            "    for (int rs_q = 0; rs_q < RS_S; ++rs_q) {",
+            "      rs_mbar_init(&rs_full[rs_q], 1);",
+            "      rs_mbar_init(&rs_empty[rs_q], RS_B / 32);",
+            "    }",
+            "    rs_fence_barrier_init();",
+            "  }",
+            "  __syncthreads();",
+        ]
+        if REDUCE_TMA_CONTIG:
+            lines += [
+                "  // a contiguous run of chunks per block: [b*NCH/G, (b+1)*NCH/G) of RS_CH4 float4 per stream",
+                "  const int rs_c0 = (int)(((long long)blockIdx.x * RS_NCH) / RS_G);",
+                "  const int rs_nmine = (int)(((long long)(blockIdx.x + 1) * RS_NCH) / RS_G) - rs_c0;",
+            ]
+            chunk_of = "rs_c0 + rs_k"
+        else:
+            lines += [
+                "  // chunks blockIdx.x, blockIdx.x + G, ... of RS_CH4 float4 per stream",
+                "  const int rs_nmine = (int)blockIdx.x < RS_NCH ? (RS_NCH - 1 - (int)blockIdx.x) / RS_G + 1 : 0;",
+            ]
+            chunk_of = "(int)blockIdx.x + rs_k * RS_G"
+        lines += [
+            "  if (threadIdx.x >= RS_B) {",
+            "    // producer warp: one lane streams the chunks through the stage ring (TMA bulk copies)",
+            "    if (threadIdx.x == RS_B) {",
+            "      for (int rs_k = 0; rs_k < rs_nmine; ++rs_k) {",
+            "        const int rs_q = rs_k % RS_S;",
+            "        if (rs_k >= RS_S) rs_mbar_wait(&rs_empty[rs_q], ((rs_k / RS_S) & 1) ^ 1);",
+            f"        const int rs_c = {chunk_of};",
+            "        const int rs_len = RS_N4 - rs_c * RS_CH4 < RS_CH4 ? RS_N4 - rs_c * RS_CH4 : RS_CH4;",
+            "        rs_mbar_arrive_expect_tx(&rs_full[rs_q], (unsigned)(rs_len * 16 * RS_NSTR));",
+        ]
+        for k in range(NSTR):
+            lines.append(f"        rs_bulk_g2s(rs_ring + (rs_q * RS_NSTR + {k}) * RS_CH4, rs_g{k} + (size_t)rs_c * RS_CH4, "
+                         "(unsigned)(rs_len * 16), &rs_full[rs_q]);")
+        lines += [
+            "      }",
+            "    }",
+            "  } else {",
+            "    // phase 1: thread t folds, chunk after chunk, float4 t, t + B, t + 2B, ... of the chunk",
+            "    for (int rs_k = 0; rs_k < rs_nmine; ++rs_k) {",
+            "      const int rs_q = rs_k % RS_S;",
+            f"      const int rs_c = {chunk_of};",
+            "      const int rs_len = RS_N4 - rs_c * RS_CH4 < RS_CH4 ? RS_N4 - rs_c * RS_CH4 : RS_CH4;",
+            "      rs_mbar_wait(&rs_full[rs_q], (rs_k / RS_S) & 1);",
+            "#pragma unroll",
+            "      for (int rs_i = 0; rs_i < (RS_CH4 + RS_B - 1) / RS_B; ++rs_i) {",
+            "        const int rs_e = threadIdx.x + rs_i * RS_B;",
+            "        if (rs_e < rs_len) {",
+        ]
+        for k in range(NSTR):
+            lines.append(f"          const float4 rs_v{k}[1] = {{rs_ring[(rs_q * RS_NSTR + {k}) * RS_CH4 + rs_e]}};")
+        for comp in ("x", "y", "z", "w"):
+            lines.append(f"          rs_acc = {add('rs_acc', term_with('0', comp))};")
+        lines += [
+            "        }",
+            "      }",
+            "      __syncwarp();",
+            "      if ((threadIdx.x & 31) == 0) rs_mbar_arrive(&rs_empty[rs_q]);",
+            "    }",
+            "  }",
+        ]
+    else:
+        lines += [
+            "  constexpr int RS_T = RS_G * RS_B;",
+            "  constexpr int RS_ITERS = (RS_N4 + RS_T - 1) / RS_T;",
+            "  const int rs_tid = blockIdx.x * blockDim.x + threadIdx.x;",
+            "  // phase 1: thread-local left fold over float4 chunks tid, tid+T, tid+2T, ...",
+            f"  for (int rs_it = 0; rs_it < RS_ITERS; rs_it += {U}) {{",
+        ]
+        for k in range(len(s_list)):
+            lines.append(f"    float4 rs_v{k}[{U}];")
+        lines += [
+            "#pragma unroll",
+            f"    for (int rs_u = 0; rs_u < {U}; ++rs_u) {{",
+            "      const int rs_c = rs_tid + (rs_it + rs_u) * RS_T;",
+            "      if (rs_it + rs_u < RS_ITERS && rs_c < RS_N4) {",
+        ]
+        for k in range(len(s_list)):
+            lines.append(f"        rs_v{k}[rs_u] = rs_ldg_stream(rs_g{k} + rs_c);")
+        lines += [
+            "      }",
+            "    }",
+            "#pragma unroll",
+            f"    for (int rs_u = 0; rs_u < {U}; ++rs_u) {{",
+            "      const int rs_c = rs_tid + (rs_it + rs_u) * RS_T;",
+            "      if (rs_it + rs_u < RS_ITERS && rs_c < RS_N4) {",
+        ]
+        for comp in ("x", "y", "z", "w"):
+            lines.append(f"        rs_acc = {add('rs_acc', term_with('rs_u', comp))};")
+        lines += [
+            "      }",
+            "    }",
+            "  }",
+        ]
+    W = B // 32
     lines += [
-        f"  {ct} rs_acc = {zero};",
-        "  // phase 1: thread-local left fold over float4 chunks tid, tid+T, tid+2T, ...",
-        f"  for (int rs_it = 0; rs_it < RS_ITERS; rs_it += {U}) {{",
-    ]
-    for k in range(len(s_list)):
-        lines.append(f"    float4 rs_v{k}[{U}];")
-    lines += [
-        "#pragma unroll",
-        f"    for (int rs_u = 0; rs_u < {U}; ++rs_u) {{",
-        "      const int rs_c = rs_tid + (rs_it + rs_u) * RS_T;",
-        "      if (rs_it + rs_u < RS_ITERS && rs_c < RS_N4) {",
-    ]
-    for k in range(len(s_list)):
-        lines.append(f"        rs_v{k}[rs_u] = rs_ldg_stream(rs_g{k} + rs_c);")
-    lines += [
-        "      }",
-        "    }",
-        "#pragma unroll",
-        f"    for (int rs_u = 0; rs_u < {U}; ++rs_u) {{",
-        "      const int rs_c = rs_tid + (rs_it + rs_u) * RS_T;",
-        "      if (rs_it + rs_u < RS_ITERS && rs_c < RS_N4) {",
-    ]
-    for comp in ("x", "y", "z", "w"):
-        lines.append(f"        rs_acc = {add('rs_acc', term_with('rs_u', comp))};")
-    lines += [
-        "      }",
-        "    }",
-        "  }",
         "  // phase 2: warp butterfly (xor 16, 8, 4, 2, 1); every lane ends with the same value",
         f"  {ct} rs_s = rs_acc;",
         "#pragma unroll",
         f"  for (int rs_o = 16; rs_o > 0; rs_o >>= 1) rs_s = {add('rs_s', shfl)};",
-        f"  __shared__ {ct} rs_w[{REDUCE_BLOCK // 32}];",
+        f"  __shared__ {ct} rs_w[{W}];",
         "  __shared__ bool rs_last;",
-        "  if ((threadIdx.x & 31) == 0) rs_w[threadIdx.x >> 5] = rs_s;",
+        "  if ((threadIdx.x & 31) == 0 && threadIdx.x < RS_B) rs_w[threadIdx.x >> 5] = rs_s;",
         "  __syncthreads();",
         "  // phase 3: block butterfly over the warp totals (warp 0)",
         "  if (threadIdx.x < 32) {",
-        f"    rs_s = threadIdx.x < {REDUCE_BLOCK // 32} ? rs_w[threadIdx.x] : {zero};",
+        f"    rs_s = threadIdx.x < {W} ? rs_w[threadIdx.x] : {zero};",
         "#pragma unroll",
         f"    for (int rs_o = 16; rs_o > 0; rs_o >>= 1) rs_s = {add('rs_s', shfl)};",
         "    if (threadIdx.x == 0) {",
         "      rs_partials[blockIdx.x] = rs_s;",
-        "      __threadfence();",
-        "      rs_last = atomicAdd(rs_ticket, 1u) == gridDim.x - 1;",
+        "      unsigned rs_prev;  // release: the partial is visible before the ticket; acquire for the last block",
+        "      asm volatile(\"atom.add.acq_rel.gpu.u32 %0, [%1], 1;\" : \"=r\"(rs_prev) : \"l\"(rs_ticket) : \"memory\");",
+        "      rs_last = rs_prev == gridDim.x - 1;",
         "    }",
         "  }",
         "  __syncthreads();",
-        "  if (!rs_last) return;",
+        "  if (!rs_last || threadIdx.x >= RS_B) return;",
         "  // phase 4 (last block): thread-strided left folds of the block partials, then butterflies",
-        "  __threadfence();",
         f"  {ct} rs_p = {zero};",
-        "  for (int rs_b = threadIdx.x; rs_b < gridDim.x; rs_b += blockDim.x) {",
+        "  for (int rs_b = threadIdx.x; rs_b < RS_G; rs_b += RS_B) {",
         f"    rs_p = {add('rs_p', '__ldcg(rs_partials + rs_b)')};",
         "  }",
         "  rs_s = rs_p;",
         "#pragma unroll",
         f"  for (int rs_o = 16; rs_o > 0; rs_o >>= 1) rs_s = {add('rs_s', shfl)};",
         "  if ((threadIdx.x & 31) == 0) rs_w[threadIdx.x >> 5] = rs_s;",
-        "  __syncthreads();",
+        "  asm volatile(\"bar.sync 1, %0;\" :: \"r\"(RS_B));  // the folding warps only",
         "  if (threadIdx.x < 32) {",
-        f"    rs_s = threadIdx.x < {REDUCE_BLOCK // 32} ? rs_w[threadIdx.x] : {zero};",
+        f"    rs_s = threadIdx.x < {W} ? rs_w[threadIdx.x] : {zero};",
         "#pragma unroll",
         f"    for (int rs_o = 16; rs_o > 0; rs_o >>= 1) rs_s = {add('rs_s', shfl)};",
         "    if (threadIdx.x == 0) {",
         f"      {ct} {acc.name} = {vr_plain(init.value)};",
         f"      {acc.name} = {add(acc.name, 'rs_s')};",
     ]
-    for s in post:
-        lines += [("      " + x) for x in thread_lines(prog, s, exact)]
+    for s_ in post:
+        lines += [("      " + x) for x in thread_lines(prog, s_, exact)]
     lines += [
         "      *rs_ticket = 0u;",
         "    }",
@@ -361,12 +461,13 @@ def _match_reduce(prog, stage, base_name, temps, exact):
     plan = {
         "name": name,
         "kind": "reduce",
-        "grid": REDUCE_GRID,
-        "block": REDUCE_BLOCK,
+        "grid": G,
+        "block": nthreads,
+        "smem": smem,
         "pre": pre,
         "fmad": False,
         "order": "reassociated",
-        "workspace": [{"name": ws_p, "ctype": ct, "size": str(REDUCE_GRID)},
+        "workspace": [{"name": ws_p, "ctype": ct, "size": str(G)},
                       {"name": ws_t, "ctype": "int", "size": "1"}],
         "extra_args": [{"kind": "workspace", "name": ws_p}, {"kind": "workspace", "name": ws_t}],
     }
@@ -374,7 +475,7 @@ def _match_reduce(prog, stage, base_name, temps, exact):
 
 
 def _launch_reduce(st, nats, sm):
-    return (st["grid"], 1, 1), (st["block"], 1, 1), 0, (1, 1, 1)
+    return (st["grid"], 1, 1), (st["block"], 1, 1), st.get("smem", 0), (1, 1, 1)
 
 
 LAUNCHERS = {

@@ -31,6 +31,7 @@ from __future__ import annotations
 from . import lir
 from ._ref import nat
 from .emit_cuda import GenericKernel, NatRenderer, Stage, ValueRenderer, kernel_head, py_expr
+from .vec2 import NoVec2, Vec2
 
 import os
 
@@ -211,8 +212,9 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     step2_lines = None
     if packed:
         try:
-            step2_lines = _Vec2(prog, gv, hook).stmt(jloop.body, 2)
-        except _NoVec2:
+            step2_lines = Vec2(prog, gv, lambda ld, _lane: hook(ld), exact=False,
+                               names=("rs_ga", "rs_gb")).stmt(jloop.body, 2)
+        except NoVec2:
             packed = False
     gp = GenericKernel(prog, Stage("serial", lir.Seq(list(post))), "_", [], exact=fast)
     post_lines = gp.thread(lir.Seq(list(post)), 3)
@@ -346,107 +348,6 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "pre": [],
     }
     return "\n".join(lines) + "\n", plan
-
-
-class _NoVec2(Exception):
-    pass
-
-
-class _Vec2:
-    """Render the fold body for two targets at once: every f32 value becomes a
-    float2 (lane x = target a, lane y = target b); target-dependent loads are
-    gathered per lane, everything else is broadcast; `a*b + c` patterns become
-    one FFMA2 (the same contraction the scalar fast path allows)."""
-
-    def __init__(self, prog, gv, hook):
-        self.prog = prog
-        self.hook = hook
-        self.gv = gv
-        self.ra = NatRenderer(prog.clamps, names={gv: "rs_ga"})
-        self.rb = NatRenderer(prog.clamps, names={gv: "rs_gb"})
-        self.r = NatRenderer(prog.clamps)
-        self.scalar_inputs = {n for n, b in prog.inputs if isinstance(b, lir.ScalarRef)}
-        self.local_arrays = set()
-
-    def val(self, e):
-        if isinstance(e, lir.Lit):
-            if e.ctype != "float":
-                raise _NoVec2()
-            return f"make_float2({e.text}, {e.text})"
-        if isinstance(e, lir.ScalarRef):
-            if e.ctype != "float":
-                raise _NoVec2()
-            if e.name in self.scalar_inputs:
-                return f"make_float2({e.name}, {e.name})"
-            return e.name
-        if isinstance(e, lir.Load):
-            if e.ctype != "float":
-                raise _NoVec2()
-            if e.buf in self.local_arrays:
-                return f"{e.buf}[{self.r(e.index)}]"
-            h = self.hook(e)
-            if h is not None:
-                return f"rs_bcast2({h})"
-            if self.gv in nat.free_vars(e.index):
-                return f"make_float2({e.buf}[{self.ra(e.index)}], {e.buf}[{self.rb(e.index)}])"
-            return f"rs_bcast2({e.buf}[{self.r(e.index)}])"
-        if isinstance(e, lir.Bin):
-            if e.ctype != "float":
-                raise _NoVec2()
-            if e.op == "+":
-                if isinstance(e.b, lir.Bin) and e.b.op == "*":
-                    return f"__ffma2_rn({self.val(e.b.a)}, {self.val(e.b.b)}, {self.val(e.a)})"
-                if isinstance(e.a, lir.Bin) and e.a.op == "*":
-                    return f"__ffma2_rn({self.val(e.a.a)}, {self.val(e.a.b)}, {self.val(e.b)})"
-                return f"__fadd2_rn({self.val(e.a)}, {self.val(e.b)})"
-            if e.op == "-":
-                if isinstance(e.a, lir.Bin) and e.a.op == "*":
-                    return f"__ffma2_rn({self.val(e.a.a)}, {self.val(e.a.b)}, rs_neg2({self.val(e.b)}))"
-                return f"__fadd2_rn({self.val(e.a)}, rs_neg2({self.val(e.b)}))"
-            if e.op == "*":
-                return f"__fmul2_rn({self.val(e.a)}, {self.val(e.b)})"
-            if e.op == "/":
-                return f"rs_div2({self.val(e.a)}, {self.val(e.b)})"
-        if isinstance(e, lir.Un):
-            if e.fn == "rsqrt":
-                return f"rs_rsqrt2({self.val(e.a)})"
-            if e.fn == "sqrt":
-                return f"rs_sqrt2({self.val(e.a)})"
-        raise _NoVec2()
-
-    def stmt(self, s, ind):
-        p = "  " * ind
-        if isinstance(s, lir.Seq):
-            out = []
-            for c in s.stmts:
-                out += self.stmt(c, ind)
-            return out
-        if isinstance(s, lir.Alloc):
-            if s.ctype != "float":
-                raise _NoVec2()
-            if s.dims:
-                self.local_arrays.add(s.name)
-                size = nat.Const(1)
-                for d in s.dims:
-                    size = size * d
-                decl = f"{p}float2 {s.name}[{self.r(nat.normalize(size))}];"
-            else:
-                decl = f"{p}float2 {s.name};"
-            return [decl] + self.stmt(s.body, ind)
-        if isinstance(s, lir.Assign):
-            t = s.target
-            if isinstance(t, lir.ScalarRef):
-                lhs = t.name
-            elif isinstance(t, lir.Store) and t.buf in self.local_arrays:
-                lhs = f"{t.buf}[{self.r(t.index)}]"
-            else:
-                raise _NoVec2()
-            return [f"{p}{lhs} = {self.val(s.value)};"]
-        if isinstance(s, lir.For):
-            pre = ["#pragma unroll"] if isinstance(s.bound, nat.Const) and s.bound.value <= 16 else []
-            head = f"{p}for (int {s.var} = 0; {s.var} < {self.r(s.bound)}; {s.var} += 1) {{"
-            return pre + [head] + self.stmt(s.body, ind + 1) + [f"{p}}}"]
-        raise _NoVec2()
 
 
 def launch(st, nats, sm):

@@ -153,9 +153,10 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     g = GenericKernel(prog, Stage("serial", body), "_", [], exact)
     g.r = ValueRenderer(prog, exact, load_hook=hook)
     body_lines = g.thread(body, 4)
+    pair_lines, store_pre = _pair_body(prog, body, rv, cv, abuf, small, hook, exact, r)
     hdim = r(nat.normalize(A.dims[0] - nat.Const(1)))
     wdim = r(nat.normalize(A.dims[1] - nat.Const(1)))
-    lines = kernel_head(prog, name, temps, launch_bounds=TX * TY,
+    lines = kernel_head(prog, name, temps, launch_bounds=f"{TX * TY}, {BLOCKS_PER_SM}",
                         extra_params=["const __grid_constant__ rs_tmap rs_map"])
     lines += [
         f"  constexpr int RS_R = {r(R)}, RS_C = {r(C)};",
@@ -176,10 +177,9 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         f"    const int tr0 = r0 + ({o0lo}), tc0 = c0 - {lp};",
         "    return tr0 >= 0 && tr0 + RS_SR <= RS_H && tc0 >= 0 && tc0 + RS_SW <= RS_W;",
         "  };",
-        "  auto rs_issue = [&](int t, int s) {  // thread 0 only",
+        "  auto rs_issue = [&](int t, int s) {  // thread 0 only; border tiles too (out-of-range cells arrive as 0)",
         "    int r0, c0;",
         "    rs_origin(t, r0, c0);",
-        "    if (!rs_is_interior(r0, c0)) return;",
         "    rs_fence_proxy_async();  // earlier generic-proxy accesses of this stage precede the TMA write",
         "    rs_mbar_arrive_expect_tx(&rs_bar[s], (unsigned)(RS_SR * RS_SW * 4));",
         f"    rs_tma_load_2d(rs_buf + s * RS_STAGE, &rs_map, c0 - {lp}, r0 + ({o0lo}), &rs_bar[s]);",
@@ -209,13 +209,24 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "    float* rs_tile = rs_buf + rs_s * RS_STAGE;",
         "    // prefetch the next tile into the other stage (freed by the barrier that ended the previous tile)",
         "    if (rs_tid == 0 && rs_t + (int)gridDim.x < RS_NTILES) rs_issue(rs_t + gridDim.x, rs_s ^ 1);",
-        "    if (rs_is_interior(rs_r0, rs_c0)) {",
-        "      if (rs_s == 0) { rs_mbar_wait(&rs_bar[0], rs_phase0); rs_phase0 ^= 1u; }",
-        "      else { rs_mbar_wait(&rs_bar[1], rs_phase1); rs_phase1 ^= 1u; }",
-        "    } else {",
+        "    if (rs_s == 0) { rs_mbar_wait(&rs_bar[0], rs_phase0); rs_phase0 ^= 1u; }",
+        "    else { rs_mbar_wait(&rs_bar[1], rs_phase1); rs_phase1 ^= 1u; }",
+        "    if (!rs_is_interior(rs_r0, rs_c0)) {",
+        "      // padClamp: every out-of-range staged cell takes the value of the nearest in-range",
+        "      // cell, which the same box holds (the box always contains an in-range row and column)",
+        "      const int rs_ylo = rs_tr0 < 0 ? -rs_tr0 : 0, rs_xlo = rs_tc0 < 0 ? -rs_tc0 : 0;",
+        f"      const int rs_yhi = {hdim} - rs_tr0, rs_xhi = {wdim} - rs_tc0;  // last in-range staged row / column",
+        "      // rows first (full width), then columns: corner cells end up clamped in both dimensions",
         f"      for (int rs_e = rs_tid; rs_e < RS_SR * RS_SW; rs_e += {TX * TY}) {{",
-        "        const int rs_y = rs_e / RS_SW, rs_x = rs_e - (rs_e / RS_SW) * RS_SW;",
-        f"        rs_tile[rs_e] = {abuf}[rs_clamp(rs_tr0 + rs_y, {hdim}) * RS_W + rs_clamp(rs_tc0 + rs_x, {wdim})];",
+        "        const int rs_y = rs_e / RS_SW, rs_x = rs_e - rs_y * RS_SW;",
+        "        if (rs_y < rs_ylo) rs_tile[rs_e] = rs_tile[rs_ylo * RS_SW + rs_x];",
+        "        else if (rs_y > rs_yhi) rs_tile[rs_e] = rs_tile[rs_yhi * RS_SW + rs_x];",
+        "      }",
+        "      __syncthreads();",
+        f"      for (int rs_e = rs_tid; rs_e < RS_SR * RS_SW; rs_e += {TX * TY}) {{",
+        "        const int rs_y = rs_e / RS_SW, rs_x = rs_e - rs_y * RS_SW;",
+        "        if (rs_x < rs_xlo) rs_tile[rs_e] = rs_tile[rs_y * RS_SW + rs_xlo];",
+        "        else if (rs_x > rs_xhi) rs_tile[rs_e] = rs_tile[rs_y * RS_SW + rs_xhi];",
         "      }",
         "      __syncthreads();",
         "    }",
@@ -241,6 +252,11 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     for guarded in (False, True):
         if not guarded:
             lines.append(f"    if (rs_r0 + {TR} <= RS_R && rs_c0 + {TC} <= RS_C) {{")
+            if pair_lines is not None:
+                # full tile: two adjacent columns per packed fp32x2 body, a
+                # row's CPT = 4 outputs leave as one 16-byte store
+                lines += pair_lines
+                continue
         else:
             lines.append("    } else {")
         lines += [
@@ -267,12 +283,72 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "blocks_per_sm": BLOCKS_PER_SM,
         "fmad": False,
         "order": "preserved",
-        "pre": [f"({py_expr(A.dims[1])}) % 4 == 0", f"({py_expr(R)}) * ({py_expr(C)}) > 0"],
+        "pre": [f"({py_expr(A.dims[1])}) % 4 == 0", f"({py_expr(R)}) * ({py_expr(C)}) > 0"] + store_pre,
+        "packed": pair_lines is not None,
         "extra_args": [{"kind": "tma2d", "buf": abuf, "offset": "0",
                         "dims": [py_expr(A.dims[1]), py_expr(A.dims[0])], "pitch": py_expr(A.dims[1]),
                         "box": [sw, sr], "swizzle": 0}],
     }
     return "\n".join(lines) + "\n", plan
+
+
+def _pair_body(prog, body, rv, cv, abuf, small, hook, exact, r):
+    """Packed fp32x2 version of the body for output columns (q, q + 1):
+    (lines of the full-tile compute, extra preconditions), or (None, [])."""
+    from .vec2 import NoVec2, Vec2
+
+    stored = []
+
+    def hook2(ld, lane):
+        h = hook(ld)
+        if h is None or ld.buf in small:
+            return h
+        return h.replace("rs_q +", "rs_qa +" if lane == 0 else "rs_qb +")
+
+    def store_hook(t, value):
+        if t.buf != prog.output.name or stored:
+            return None
+        idx = nat.normalize(t.index)
+        z = {cv: nat.Const(0), rv: nat.Const(0)}
+        at = lambda a, b: nat.normalize(nat.substitute(idx, {rv: nat.Const(a), cv: nat.Const(b)}))  # noqa: E731
+        base = nat.normalize(nat.substitute(idx, {cv: nat.Const(0)}))
+        one = nat.normalize(at(0, 1) - at(0, 0))
+        if not (isinstance(one, nat.Const) and one.value == 1) or cv in nat.free_vars(base):
+            return None
+        stored.append((base, nat.normalize(at(1, 0) - at(0, 0)), nat.normalize(nat.substitute(idx, z))))
+        return [f"rs_o2 = {value};"]
+
+    try:
+        v = Vec2(prog, cv, hook2, exact=exact, store_hook=store_hook)
+        blines = v.stmt(body, 4)
+    except NoVec2:
+        return None, []
+    if len(stored) != 1:
+        return None, []
+    base, row_coef, const = stored[0]
+    if nat.free_vars(row_coef) - set(prog.nat_params) or nat.free_vars(const) - set(prog.nat_params):
+        return None, []
+    pre = [f"({py_expr(row_coef)}) % 4 == 0", f"({py_expr(const)}) % 4 == 0"]
+    out = prog.output.name
+    lines = [
+        "    auto rs_pair = [&](const int rs_k, const int rs_qa, const int rs_qb) -> float2 {",
+        f"      const int {rv} = rs_r0 + threadIdx.y * {RPT} + rs_k;",
+        f"      const int rs_la = rs_c0 + threadIdx.x * {CPT} + rs_qa, rs_lb = rs_c0 + threadIdx.x * {CPT} + rs_qb;",
+        "      float2 rs_o2;",
+    ]
+    lines += blines
+    lines += [
+        "      return rs_o2;",
+        "    };",
+        "#pragma unroll",
+        f"    for (int rs_k = 0; rs_k < {RPT}; ++rs_k) {{",
+        f"      const int {rv} = rs_r0 + threadIdx.y * {RPT} + rs_k;",
+        "      const float2 rs_lo = rs_pair(rs_k, 0, 1), rs_hi = rs_pair(rs_k, 2, 3);",
+        f"      *reinterpret_cast<float4*>(&{out}[({r(base)}) + rs_c0 + threadIdx.x * {CPT}]) = "
+        "make_float4(rs_lo.x, rs_lo.y, rs_hi.x, rs_hi.y);",
+        "    }",
+    ]
+    return lines, pre
 
 
 def launch(st, nats, sm):

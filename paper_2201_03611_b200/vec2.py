@@ -1,0 +1,164 @@
+"""Packed fp32x2 rendering of a thread body: two instances of the same
+computation (two "lanes", e.g. two target bodies or two adjacent output
+columns) run as one stream of FADD2 / FMUL2 / FFMA2 instructions.
+
+On sm_100 a packed fp32x2 instruction issues at the same rate as a scalar
+FFMA (B300_MICROARCH.md "Pipe rates": rt 2 per SMSP) but does two lanes'
+work, so the FP32 pipe's peak is only reachable with packed arithmetic.
+
+Every f32 value of the body becomes a float2 (x = lane a, y = lane b).
+Loads are resolved by `hook(load, lane)` (template-specific staging, returns
+a string or None); an unhooked load whose index depends on `lane_var` is
+gathered per lane (the lane variable renamed to `names[0]` / `names[1]`),
+any other load is broadcast.
+
+exact=True keeps the reference's fp32 semantics bit for bit: each
+operation is correctly rounded per lane and never contracted — adds are
+__fadd2_rn, products rs_fmul2_exact (device.cuh: ptxas fuses a packed
+mul + add into FFMA2 even with -fmad=false, so the product is an FFMA2
+with an opaque -0.0 addend).  The one rewrite is
+`s = (+0.0) + a*b` -> `__ffma2_rn(a, b, +0.0)`, exact because a fused
+multiply-add with a +0.0 addend rounds once, like the multiply, and then
+adds +0.0 (which maps -0.0 to +0.0 exactly as the separate add does).
+Constant-trip loops are unrolled here (so the first step of a fold from
+0.0f is visible); scalars are tracked as "known +0.0" only until their next
+assignment.
+
+exact=False (fast math) additionally contracts `a*b + c` into FFMA2.
+"""
+
+from __future__ import annotations
+
+from . import lir
+from ._ref import nat
+from .emit_cuda import NatRenderer
+
+UNROLL_MAX = 16
+
+
+class NoVec2(Exception):
+    pass
+
+
+class Vec2:
+    def __init__(self, prog, lane_var, hook, *, exact, names=("rs_la", "rs_lb"), store_hook=None):
+        self.prog = prog
+        self.lane_var = lane_var
+        self.hook = hook
+        self.exact = exact
+        self.store_hook = store_hook  # (Store, value_str) -> [lines] or None
+        self.ra = NatRenderer(prog.clamps, names={lane_var: names[0]})
+        self.rb = NatRenderer(prog.clamps, names={lane_var: names[1]})
+        self.r = NatRenderer(prog.clamps)
+        self.scalar_inputs = {n for n, b in prog.inputs if isinstance(b, lir.ScalarRef)}
+        self.local_arrays = set()
+        self.zero = set()  # scalars currently known to hold +0.0
+
+    # ---- values ---------------------------------------------------------
+
+    def val(self, e):
+        if isinstance(e, lir.Lit):
+            if e.ctype != "float":
+                raise NoVec2()
+            return f"make_float2({e.text}, {e.text})"
+        if isinstance(e, lir.ScalarRef):
+            if e.ctype != "float":
+                raise NoVec2()
+            if e.name in self.scalar_inputs:
+                return f"make_float2({e.name}, {e.name})"
+            return e.name
+        if isinstance(e, lir.Load):
+            if e.ctype != "float":
+                raise NoVec2()
+            if e.buf in self.local_arrays:
+                return f"{e.buf}[{self.r(e.index)}]"
+            ha, hb = self.hook(e, 0), self.hook(e, 1)
+            if ha is not None:
+                return f"rs_bcast2({ha})" if ha == hb else f"make_float2({ha}, {hb})"
+            if self.lane_var in nat.free_vars(e.index):
+                return f"make_float2({e.buf}[{self.ra(e.index)}], {e.buf}[{self.rb(e.index)}])"
+            return f"rs_bcast2({e.buf}[{self.r(e.index)}])"
+        if isinstance(e, lir.Bin):
+            if e.ctype != "float":
+                raise NoVec2()
+            if e.op == "+":
+                if not self.exact:
+                    if isinstance(e.b, lir.Bin) and e.b.op == "*":
+                        return f"__ffma2_rn({self.val(e.b.a)}, {self.val(e.b.b)}, {self.val(e.a)})"
+                    if isinstance(e.a, lir.Bin) and e.a.op == "*":
+                        return f"__ffma2_rn({self.val(e.a.a)}, {self.val(e.a.b)}, {self.val(e.b)})"
+                elif self._is_zero(e.a) and isinstance(e.b, lir.Bin) and e.b.op == "*":
+                    return f"__ffma2_rn({self.val(e.b.a)}, {self.val(e.b.b)}, make_float2(0.0f, 0.0f))"
+                return f"__fadd2_rn({self.val(e.a)}, {self.val(e.b)})"
+            if e.op == "-":
+                if not self.exact and isinstance(e.a, lir.Bin) and e.a.op == "*":
+                    return f"__ffma2_rn({self.val(e.a.a)}, {self.val(e.a.b)}, rs_neg2({self.val(e.b)}))"
+                return f"__fadd2_rn({self.val(e.a)}, rs_neg2({self.val(e.b)}))"
+            if e.op == "*":
+                fn = "rs_fmul2_exact" if self.exact else "__fmul2_rn"
+                return f"{fn}({self.val(e.a)}, {self.val(e.b)})"
+            if e.op == "/":
+                return f"rs_div2({self.val(e.a)}, {self.val(e.b)})" if not self.exact else \
+                    f"rs_div2_rn({self.val(e.a)}, {self.val(e.b)})"
+        if isinstance(e, lir.Un):
+            if e.fn == "rsqrt":
+                return f"rs_rsqrt2({self.val(e.a)})" if not self.exact else f"rs_rsqrt2_rn({self.val(e.a)})"
+            if e.fn == "sqrt":
+                return f"rs_sqrt2({self.val(e.a)})" if not self.exact else f"rs_sqrt2_rn({self.val(e.a)})"
+        raise NoVec2()
+
+    def _is_zero(self, e):
+        if isinstance(e, lir.ScalarRef):
+            return e.name in self.zero
+        return isinstance(e, lir.Lit) and e.text in ("0.0f", "0.0")
+
+    # ---- statements -----------------------------------------------------
+
+    def stmt(self, s, ind):
+        p = "  " * ind
+        if isinstance(s, lir.Seq):
+            out = []
+            for c in s.stmts:
+                out += self.stmt(c, ind)
+            return out
+        if isinstance(s, lir.Alloc):
+            if s.ctype != "float":
+                raise NoVec2()
+            if s.dims:
+                self.local_arrays.add(s.name)
+                size = nat.Const(1)
+                for d in s.dims:
+                    size = size * d
+                decl = f"{p}float2 {s.name}[{self.r(nat.normalize(size))}];"
+            else:
+                decl = f"{p}float2 {s.name};"
+            return [decl] + self.stmt(s.body, ind)
+        if isinstance(s, lir.Assign):
+            t = s.target
+            value = self.val(s.value)
+            if isinstance(t, lir.ScalarRef):
+                self.zero.discard(t.name)
+                if isinstance(s.value, lir.Lit) and s.value.text in ("0.0f", "0.0"):
+                    self.zero.add(t.name)
+                return [f"{p}{t.name} = {value};"]
+            if isinstance(t, lir.Store) and t.buf in self.local_arrays:
+                return [f"{p}{t.buf}[{self.r(t.index)}] = {value};"]
+            if isinstance(t, lir.Store) and self.store_hook is not None:
+                out = self.store_hook(t, value)
+                if out is not None:
+                    return [p + x for x in out]
+            raise NoVec2()
+        if isinstance(s, lir.For):
+            if isinstance(s.bound, nat.Const) and s.bound.value <= UNROLL_MAX:
+                out = []
+                for k in range(s.bound.value):
+                    out.append(f"{p}{{ const int {s.var} = {k};")
+                    out += self.stmt(s.body, ind + 1)
+                    out.append(f"{p}}}")
+                return out
+            self.zero.clear()
+            head = f"{p}for (int {s.var} = 0; {s.var} < {self.r(s.bound)}; {s.var} += 1) {{"
+            body = self.stmt(s.body, ind + 1)
+            self.zero.clear()
+            return [head] + body + [f"{p}}}"]
+        raise NoVec2()

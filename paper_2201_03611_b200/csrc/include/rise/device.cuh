@@ -122,6 +122,20 @@ RS_DEVICE void rs_tma_load_2d(void* dst, const rs_tmap* map, int c0, int c1, uns
       : "memory");
 }
 
+// 2-D TMA tile store shared -> global (out-of-range box elements are not
+// written), tracked as a bulk async-group of the issuing thread.
+RS_DEVICE void rs_tma_store_2d(const rs_tmap* map, int c0, int c1, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<unsigned long long>(map)),
+               "r"(c0), "r"(c1), "r"(rs_smem_addr(src))
+               : "memory");
+}
+RS_DEVICE void rs_bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the shared-memory sources of every committed bulk store have been read
+RS_DEVICE void rs_bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// every committed bulk store has completed
+RS_DEVICE void rs_bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // 128-bit streaming global load that does not allocate in L1.
 RS_DEVICE float4 rs_ldg_stream(const float4* p) {
   float4 r;

@@ -39,6 +39,8 @@ import os  # noqa: E402
 
 # persistent blocks per SM (each holds two 36 KB stages); overridable for sweeps
 BLOCKS_PER_SM = int(os.environ.get("RISE_STENCIL_BPS", "3"))
+# full tiles leave through shared memory and one TMA tile store (else 16-byte STGs)
+TMA_STORE = os.environ.get("RISE_STENCIL_TMA_STORE", "1") == "1"
 
 
 def _seq_loop_bounds(stmt):
@@ -153,11 +155,14 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     g = GenericKernel(prog, Stage("serial", body), "_", [], exact)
     g.r = ValueRenderer(prog, exact, load_hook=hook)
     body_lines = g.thread(body, 4)
-    pair_lines, store_pre = _pair_body(prog, body, rv, cv, abuf, small, hook, exact, r)
+    pair_lines, store_pre, ostore = _pair_body(prog, body, rv, cv, abuf, small, hook, exact, r, TMA_STORE)
+    tma_store = ostore is not None
     hdim = r(nat.normalize(A.dims[0] - nat.Const(1)))
     wdim = r(nat.normalize(A.dims[1] - nat.Const(1)))
-    lines = kernel_head(prog, name, temps, launch_bounds=f"{TX * TY}, {BLOCKS_PER_SM}",
-                        extra_params=["const __grid_constant__ rs_tmap rs_map"])
+    params = ["const __grid_constant__ rs_tmap rs_map"]
+    if tma_store:
+        params.append("const __grid_constant__ rs_tmap rs_omap")
+    lines = kernel_head(prog, name, temps, launch_bounds=f"{TX * TY}, {BLOCKS_PER_SM}", extra_params=params)
     lines += [
         f"  constexpr int RS_R = {r(R)}, RS_C = {r(C)};",
         f"  constexpr int RS_H = {r(A.dims[0])}, RS_W = {r(A.dims[1])};",
@@ -208,7 +213,10 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         f"    const int rs_tr0 = rs_r0 + ({o0lo}), rs_tc0 = rs_c0 - {lp};",
         "    float* rs_tile = rs_buf + rs_s * RS_STAGE;",
         "    // prefetch the next tile into the other stage (freed by the barrier that ended the previous tile)",
-        "    if (rs_tid == 0 && rs_t + (int)gridDim.x < RS_NTILES) rs_issue(rs_t + gridDim.x, rs_s ^ 1);",
+        "    if (rs_tid == 0 && rs_t + (int)gridDim.x < RS_NTILES) {",
+        "      rs_bulk_wait_read_all();  // that stage staged the previous tile's output (TMA store)" if tma_store else "",
+        "      rs_issue(rs_t + gridDim.x, rs_s ^ 1);",
+        "    }",
         "    if (rs_s == 0) { rs_mbar_wait(&rs_bar[0], rs_phase0); rs_phase0 ^= 1u; }",
         "    else { rs_mbar_wait(&rs_bar[1], rs_phase1); rs_phase1 ^= 1u; }",
         "    if (!rs_is_interior(rs_r0, rs_c0)) {",
@@ -270,7 +278,11 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         ]
         lines += ["  " + x for x in body_lines]
         lines += ["        }", "      }", "    }"]
-    lines += ["    }", "  }", "}"]
+    lines += ["    }", "  }"]
+    if tma_store:
+        lines.append("  if (rs_tid == 0) rs_bulk_wait_all();  // the last tile's store has left shared memory")
+    lines += ["}"]
+    lines = [x for x in lines if x != ""]
     smem = 2 * (-(-(sr * sw) // 32) * 32) * 4 + 16 + 128
     plan = {
         "name": name,
@@ -289,12 +301,19 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
                         "dims": [py_expr(A.dims[1]), py_expr(A.dims[0])], "pitch": py_expr(A.dims[1]),
                         "box": [sw, sr], "swizzle": 0}],
     }
+    if tma_store:
+        row_coef, const = ostore
+        plan["extra_args"].append({"kind": "tma2d", "buf": prog.output.name, "offset": py_expr(const),
+                                   "dims": [py_expr(C), py_expr(R)], "pitch": py_expr(row_coef),
+                                   "box": [TC, TR], "swizzle": 0})
+        plan["tma_store"] = True
     return "\n".join(lines) + "\n", plan
 
 
-def _pair_body(prog, body, rv, cv, abuf, small, hook, exact, r):
+def _pair_body(prog, body, rv, cv, abuf, small, hook, exact, r, tma_store):
     """Packed fp32x2 version of the body for output columns (q, q + 1):
-    (lines of the full-tile compute, extra preconditions), or (None, [])."""
+    (lines of the full-tile compute, extra preconditions, (row pitch, offset)
+    of the output when it leaves by TMA store else None), or (None, [], None)."""
     from .vec2 import NoVec2, Vec2
 
     stored = []
@@ -322,12 +341,12 @@ def _pair_body(prog, body, rv, cv, abuf, small, hook, exact, r):
         v = Vec2(prog, cv, hook2, exact=exact, store_hook=store_hook)
         blines = v.stmt(body, 4)
     except NoVec2:
-        return None, []
+        return None, [], None
     if len(stored) != 1:
-        return None, []
+        return None, [], None
     base, row_coef, const = stored[0]
     if nat.free_vars(row_coef) - set(prog.nat_params) or nat.free_vars(const) - set(prog.nat_params):
-        return None, []
+        return None, [], None
     pre = [f"({py_expr(row_coef)}) % 4 == 0", f"({py_expr(const)}) % 4 == 0"]
     out = prog.output.name
     lines = [
@@ -344,11 +363,28 @@ def _pair_body(prog, body, rv, cv, abuf, small, hook, exact, r):
         f"    for (int rs_k = 0; rs_k < {RPT}; ++rs_k) {{",
         f"      const int {rv} = rs_r0 + threadIdx.y * {RPT} + rs_k;",
         "      const float2 rs_lo = rs_pair(rs_k, 0, 1), rs_hi = rs_pair(rs_k, 2, 3);",
+    ]
+    if tma_store:
+        # the stage is free once every thread holds its window: stage the
+        # output tile there ([TR][TC], conflict-free STS.128) for one TMA store
+        lines += [
+            f"      *reinterpret_cast<float4*>(&rs_tile[(threadIdx.y * {RPT} + rs_k) * {TC} + threadIdx.x * {CPT}]) = "
+            "make_float4(rs_lo.x, rs_lo.y, rs_hi.x, rs_hi.y);",
+            "    }",
+            "    rs_fence_proxy_async();  // the generic-proxy writes precede the TMA read",
+            "    __syncthreads();",
+            "    if (rs_tid == 0) {",
+            "      rs_tma_store_2d(&rs_omap, rs_c0, rs_r0, rs_tile);",
+            "      rs_bulk_commit();",
+            "    }",
+        ]
+        return lines, pre, (row_coef, const)
+    lines += [
         f"      *reinterpret_cast<float4*>(&{out}[({r(base)}) + rs_c0 + threadIdx.x * {CPT}]) = "
         "make_float4(rs_lo.x, rs_lo.y, rs_hi.x, rs_hi.y);",
         "    }",
     ]
-    return lines, pre
+    return lines, pre, None
 
 
 def launch(st, nats, sm):

@@ -450,7 +450,9 @@ def run_ours(args, rank, world, local_rank):
                 "kernels": exe.kernel_names,
                 "templates": exe.template_kinds,
                 "l2": "flushed between steps (256 MiB write + 256 MiB read sweep, outside the events)",
-                "parallelism": _parallelism_text(wl, world),
+                "parallelism": _parallelism_text(wl, world) + (
+                    "" if dist is None or dist.get_backend() == "nccl"
+                    else " [gloo test run: collectives host-staged]"),
             },
             "e2e": {"value": round(total_work / (e2e_ms * 1e-3) / 1e9, 3), "unit": wl.metric_unit,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -474,10 +476,12 @@ def _parallelism_text(wl, world):
         "gemv": f"weak: rank r owns an 8192-row band of an ({world}x8192) x 8192 matrix, x replicated, y sharded",
         "gemv_opt": f"weak: rank r owns an 8192-row band of an ({world}x8192) x 8192 matrix, x replicated",
         "sgemm": f"weak: rank r owns a 4096-row block of A ({world}x4096 rows), B replicated",
-        "dot": "weak: rank r owns a 2^24 chunk; partials all-gathered (NCCL) and folded in rank order",
-        "dot_chunked": "weak: rank r owns a 2^24 chunk; partials all-gathered (NCCL) and folded in rank order",
-        "conv": "weak: rank r owns an 8192-row band; halo rows exchanged with neighbours (NCCL P2P) per step",
-        "nbody": f"strong: 131072 bodies, {131072 // world} targets per rank; positions/masses all-gathered per step",
+        "dot": "weak: rank r owns a 2^24 chunk; partials all-gathered (rs_allgather, NCCL) and folded in rank order",
+        "dot_chunked": "weak: rank r owns a 2^24 chunk; partials all-gathered (rs_allgather, NCCL), rank-order fold",
+        "conv": "weak: rank r owns an 8192-row band; halo rows pulled from the neighbours' bands over NVLink "
+                "(rs_halo_exchange, CUDA IPC) per step",
+        "nbody": f"strong: 131072 bodies, {131072 // world} targets per rank; positions/masses all-gathered "
+                 "(rs_allgather, NCCL) per step",
     }[wl.key]
 
 
@@ -528,16 +532,31 @@ def _distributed_step(wl, exe, dev_in, out, stream, dist, rank, world):
             bound()
 
     exe = _Exe()
+    # NCCL runs: the data path goes through the native runtime's collectives
+    # (rs_allgather over NCCL, rs_halo_exchange over peer memory); gloo runs
+    # (CPU test path, several ranks per GPU) move host-staged tensors
+    native = dist.get_backend() == "nccl"
+    comm = None
+    if native and wl.key in ("dot", "dot_chunked", "nbody"):
+        from paper_2201_03611_b200 import shard
+
+        comm = shard.DeviceComm()
     if wl.key in ("dot", "dot_chunked"):
         parts = [torch.empty(1, dtype=torch.float32, device="cuda") for _ in range(world)]
+        flat = torch.empty(world, dtype=torch.float32, device="cuda")
         total = torch.empty(1, dtype=torch.float32, device="cuda")
 
         def step():
             exe(*dev_in, out=out, stream=stream)
             with torch.cuda.stream(stream):
-                dist.all_gather(parts, out)
-                total.copy_(parts[0])
-                for p in parts[1:]:  # rank-order fold (never an all-reduce)
+                if comm is not None:
+                    comm.allgather(out[:1], flat, stream)
+                    gathered = list(flat.view(world, 1).unbind(0))
+                else:
+                    dist.all_gather(parts, out)
+                    gathered = parts
+                total.copy_(gathered[0])
+                for p in gathered[1:]:  # rank-order fold (never an all-reduce)
                     total.add_(p)
 
         return step
@@ -546,8 +565,22 @@ def _distributed_step(wl, exe, dev_in, out, stream, dist, rank, world):
         m = exe.nats["m"]
         local = img.view(-1, m)
 
-        host_staged = dist.get_backend() != "nccl"  # gloo P2P moves CPU tensors only (test path)
+        host_staged = not native  # gloo P2P moves CPU tensors only (test path)
         stage = torch.empty((4, m), dtype=torch.float32) if host_staged else None
+        if native or os.environ.get("RISE_PEER_HALO", "1") == "1":
+            # peer-memory halo needs no collective backend (IPC works between
+            # processes on one GPU too, which is how it is tested here)
+            from paper_2201_03611_b200 import shard
+
+            torch.cuda.synchronize()
+            dist.barrier()
+            halo = shard.PeerHalo(local)
+
+            def step():  # pull the neighbours' edge rows over NVLink, then the stencil
+                halo.exchange(stream)
+                exe(*dev_in, out=out, stream=stream)
+
+            return step
 
         def step():
             with torch.cuda.stream(stream):
@@ -581,8 +614,12 @@ def _distributed_step(wl, exe, dev_in, out, stream, dist, rank, world):
 
         def step():
             with torch.cuda.stream(stream):
-                dist.all_gather(pos_parts, tpos)
-                dist.all_gather(mass_parts, mass_block)
+                if comm is not None:
+                    comm.allgather(tpos, pos, stream)
+                    comm.allgather(mass_block, mass, stream)
+                else:
+                    dist.all_gather(pos_parts, tpos)
+                    dist.all_gather(mass_parts, mass_block)
             exe(*dev_in, out=out, stream=stream)
 
         return step

@@ -136,6 +136,42 @@ int rs_tma_desc_2d_f32(void* desc, const void* base,
                        uint64_t dim0, uint64_t dim1, uint64_t row_stride_bytes,
                        uint32_t box0, uint32_t box1, int swizzle);
 
+/* ---- multi-GPU: peer memory and collectives (SURVEY.md §8 e) --------
+ * The reference runs on one (sequentialised) device; nothing is replaced.
+ * One process per GPU.  Out-of-band exchange of the opaque handles / ids
+ * below is the caller's plumbing (torch.distributed in the Python side). */
+
+/* Cross-process peer memory over NVLink: export the allocation holding
+ * `dptr` as a 64-byte CUDA IPC handle plus the byte offset of `dptr` in it. */
+int rs_ipc_handle(void* handle_out /* 64 bytes */, size_t* offset_out, const void* dptr);
+/* Map a peer's exported allocation into this process (peer access enabled
+ * lazily); *dptr_out = mapped base + offset.  Same-process handles fail. */
+int rs_ipc_open(void** dptr_out, const void* handle /* 64 bytes */, size_t offset);
+/* Unmap a pointer returned by rs_ipc_open. */
+int rs_ipc_close(void* dptr);
+
+/* Halo exchange of a row band laid out [rows + 2][row_bytes]: rows 1..rows
+ * are this rank's; row 0 receives the LAST owned row of the band above
+ * (`above`, its band base as mapped by rs_ipc_open, holding `above_rows`
+ * owned rows) and row rows+1 the FIRST owned row of the band below
+ * (`below`).  A NULL neighbour is a global edge: the halo row is the clamped
+ * copy of the band's own edge row (padClamp2D semantics, the halo rows of
+ * shard.halo_exchange_rows).  Enqueued on `stream` as device-to-device
+ * copies (NVLink for peers); the caller orders them after the neighbours'
+ * producers (e.g. a barrier) — a pull model, no send side. */
+int rs_halo_exchange(void* band, size_t row_bytes, size_t rows, const void* above, size_t above_rows,
+                     const void* below, void* stream);
+
+/* NCCL communicator (libnccl.so.2 is loaded at run time). */
+typedef struct rs_comm_s* rs_comm;
+/* A fresh 128-byte ncclUniqueId (rank 0 creates it, every rank passes it). */
+int rs_comm_unique_id(void* id_out /* 128 bytes */);
+int rs_comm_init(rs_comm* out, int nranks, int rank, const void* id /* 128 bytes */);
+int rs_comm_destroy(rs_comm comm);
+/* recv[r * bytes_per_rank ...] = rank r's send buffer, for every rank r, in
+ * rank order (the dot partials and the nbody positions of shard.py). */
+int rs_allgather(rs_comm comm, const void* send, void* recv, size_t bytes_per_rank, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -74,6 +74,10 @@ struct Driver {
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
   CUresult (*GetErrorString)(CUresult, const char**);
+  CUresult (*IpcGetMemHandle)(CUipcMemHandle*, CUdeviceptr);
+  CUresult (*IpcOpenMemHandle)(CUdeviceptr*, CUipcMemHandle, unsigned);
+  CUresult (*IpcCloseMemHandle)(CUdeviceptr);
+  CUresult (*MemGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
 };
 
 Driver g_drv;
@@ -123,6 +127,10 @@ int load_driver() {
   ok &= sym(g_drv.EventElapsedTime, "cuEventElapsedTime");
   ok &= sym(g_drv.TensorMapEncodeTiled, "cuTensorMapEncodeTiled");
   ok &= sym(g_drv.GetErrorString, "cuGetErrorString");
+  ok &= sym(g_drv.IpcGetMemHandle, "cuIpcGetMemHandle");
+  ok &= sym(g_drv.IpcOpenMemHandle, "cuIpcOpenMemHandle_v2");
+  ok &= sym(g_drv.IpcCloseMemHandle, "cuIpcCloseMemHandle");
+  ok &= sym(g_drv.MemGetAddressRange, "cuMemGetAddressRange_v2");
   if (!ok) return fail("rs_init: the CUDA driver lacks a required entry point");
   g_drv.loaded = true;
   return 0;
@@ -139,6 +147,50 @@ int cu_check(CUresult r, const char* what) {
   do {                                         \
     if (int _e = cu_check((call), (what))) return _e; \
   } while (0)
+
+// ---- NCCL (dlopen'd; the soname resolves to the copy already loaded by
+// the process, e.g. torch's, or the system one) ----------------------------
+struct NcclId {
+  char internal[128];
+};
+struct Nccl {
+  bool loaded = false;
+  void* handle = nullptr;
+  int (*GetUniqueId)(NcclId*);
+  int (*CommInitRank)(void**, int, NcclId, int);
+  int (*CommDestroy)(void*);
+  int (*AllGather)(const void*, void*, size_t, int, void*, CUstream);
+  const char* (*GetErrorString)(int);
+};
+Nccl g_nccl;
+constexpr int kNcclUint8 = 1;
+
+int load_nccl() {
+  if (g_nccl.loaded) return 0;
+  const char* env = getenv("RISE_NCCL_LIB");
+  const char* names[] = {env ? env : "libnccl.so.2", "libnccl.so.2", "libnccl.so"};
+  for (const char* n : names) {
+    g_nccl.handle = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+    if (g_nccl.handle) break;
+  }
+  if (!g_nccl.handle) return fail("rs_comm: cannot load NCCL (libnccl.so.2): %s", dlerror());
+  auto get = [](const char* name) { return dlsym(g_nccl.handle, name); };
+  g_nccl.GetUniqueId = reinterpret_cast<int (*)(NcclId*)>(get("ncclGetUniqueId"));
+  g_nccl.CommInitRank = reinterpret_cast<int (*)(void**, int, NcclId, int)>(get("ncclCommInitRank"));
+  g_nccl.CommDestroy = reinterpret_cast<int (*)(void*)>(get("ncclCommDestroy"));
+  g_nccl.AllGather = reinterpret_cast<int (*)(const void*, void*, size_t, int, void*, CUstream)>(get("ncclAllGather"));
+  g_nccl.GetErrorString = reinterpret_cast<const char* (*)(int)>(get("ncclGetErrorString"));
+  if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.CommDestroy || !g_nccl.AllGather ||
+      !g_nccl.GetErrorString)
+    return fail("rs_comm: the NCCL library lacks a required entry point");
+  g_nccl.loaded = true;
+  return 0;
+}
+
+int nccl_check(int r, const char* what) {
+  if (r == 0) return 0;
+  return fail("%s failed: %s (ncclResult %d)", what, g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?", r);
+}
 
 int ensure_ctx() {
   if (!g_inited) return fail("rs_init has not been called");
@@ -483,6 +535,116 @@ int rs_tma_desc_2d_f32(void* desc, const void* base, uint64_t dim0, uint64_t dim
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
      "cuTensorMapEncodeTiled");
   return 0;
+}
+
+// ---- multi-GPU ------------------------------------------------------------
+
+struct rs_comm_s {
+  void* nccl = nullptr;
+  int nranks = 0, rank = 0;
+};
+
+namespace {
+std::mutex g_ipc_mu;
+std::vector<std::pair<CUdeviceptr, CUdeviceptr>> g_ipc_open;  // (returned pointer, mapped base)
+}  // namespace
+
+int rs_ipc_handle(void* handle_out, size_t* offset_out, const void* dptr) {
+  if (int e = ensure_ctx()) return e;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  CU(g_drv.MemGetAddressRange(&base, &size, (CUdeviceptr)dptr), "cuMemGetAddressRange");
+  CUipcMemHandle h;
+  CU(g_drv.IpcGetMemHandle(&h, base), "cuIpcGetMemHandle");
+  static_assert(sizeof(CUipcMemHandle) == 64, "CUipcMemHandle is 64 bytes");
+  memcpy(handle_out, &h, sizeof(h));
+  *offset_out = (size_t)((CUdeviceptr)dptr - base);
+  return 0;
+}
+
+int rs_ipc_open(void** dptr_out, const void* handle, size_t offset) {
+  if (int e = ensure_ctx()) return e;
+  CUipcMemHandle h;
+  memcpy(&h, handle, sizeof(h));
+  CUdeviceptr base = 0;
+  CU(g_drv.IpcOpenMemHandle(&base, h, CU_IPC_MEM_LAZY_ENABLE_PEER_ACCESS), "cuIpcOpenMemHandle");
+  std::lock_guard<std::mutex> lock(g_ipc_mu);
+  g_ipc_open.emplace_back(base + offset, base);
+  *dptr_out = (void*)(base + offset);
+  return 0;
+}
+
+int rs_ipc_close(void* dptr) {
+  if (int e = ensure_ctx()) return e;
+  CUdeviceptr base = 0;
+  {
+    std::lock_guard<std::mutex> lock(g_ipc_mu);
+    for (size_t i = 0; i < g_ipc_open.size(); ++i) {
+      if (g_ipc_open[i].first == (CUdeviceptr)dptr) {
+        base = g_ipc_open[i].second;
+        g_ipc_open.erase(g_ipc_open.begin() + (long)i);
+        break;
+      }
+    }
+  }
+  if (!base) return fail("rs_ipc_close: %p was not returned by rs_ipc_open", dptr);
+  CU(g_drv.IpcCloseMemHandle(base), "cuIpcCloseMemHandle");
+  return 0;
+}
+
+int rs_halo_exchange(void* band, size_t row_bytes, size_t rows, const void* above, size_t above_rows,
+                     const void* below, void* stream) {
+  if (int e = ensure_ctx()) return e;
+  if (rows == 0) return fail("rs_halo_exchange: empty band");
+  if (above && above_rows == 0) return fail("rs_halo_exchange: the band above owns no rows");
+  const CUdeviceptr b = (CUdeviceptr)band;
+  const CUstream st = (CUstream)stream;
+  // row 0 <- last owned row of the band above (or this band's row 1)
+  const CUdeviceptr top_src = above ? (CUdeviceptr)above + above_rows * row_bytes : b + row_bytes;
+  CU(g_drv.MemcpyDtoDAsync(b, top_src, row_bytes, st), "cuMemcpyDtoDAsync (halo above)");
+  // row rows+1 <- first owned row of the band below (or this band's row `rows`)
+  const CUdeviceptr bot_src = below ? (CUdeviceptr)below + row_bytes : b + rows * row_bytes;
+  CU(g_drv.MemcpyDtoDAsync(b + (rows + 1) * row_bytes, bot_src, row_bytes, st), "cuMemcpyDtoDAsync (halo below)");
+  return 0;
+}
+
+int rs_comm_unique_id(void* id_out) {
+  if (int e = load_nccl()) return e;
+  NcclId id;
+  if (int e = nccl_check(g_nccl.GetUniqueId(&id), "ncclGetUniqueId")) return e;
+  memcpy(id_out, &id, sizeof(id));
+  return 0;
+}
+
+int rs_comm_init(rs_comm* out, int nranks, int rank, const void* id) {
+  if (int e = ensure_ctx()) return e;
+  if (int e = load_nccl()) return e;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail("rs_comm_init: rank %d of %d", rank, nranks);
+  NcclId nid;
+  memcpy(&nid, id, sizeof(nid));
+  void* c = nullptr;
+  if (int e = nccl_check(g_nccl.CommInitRank(&c, nranks, nid, rank), "ncclCommInitRank")) return e;
+  rs_comm h = new rs_comm_s;
+  h->nccl = c;
+  h->nranks = nranks;
+  h->rank = rank;
+  *out = h;
+  return 0;
+}
+
+int rs_comm_destroy(rs_comm comm) {
+  if (!comm) return 0;
+  if (int e = ensure_ctx()) return e;
+  int r = g_nccl.CommDestroy(comm->nccl);
+  delete comm;
+  return nccl_check(r, "ncclCommDestroy");
+}
+
+int rs_allgather(rs_comm comm, const void* send, void* recv, size_t bytes_per_rank, void* stream) {
+  if (!comm) return fail("rs_allgather: no communicator");
+  if (int e = ensure_ctx()) return e;
+  return nccl_check(g_nccl.AllGather(send, recv, bytes_per_rank, kNcclUint8, comm->nccl, (CUstream)stream),
+                    "ncclAllGather");
 }
 
 }  // extern "C"

@@ -33,7 +33,8 @@ EXPORTED = (
     "rs_memcpy_dtoh", "rs_memcpy_dtod", "rs_memset_d8", "rs_stream_create",
     "rs_stream_destroy", "rs_stream_synchronize", "rs_device_synchronize", "rs_event_create",
     "rs_event_destroy", "rs_event_record", "rs_event_synchronize", "rs_event_elapsed_ms",
-    "rs_tma_desc_2d_f32",
+    "rs_tma_desc_2d_f32", "rs_ipc_handle", "rs_ipc_open", "rs_ipc_close", "rs_halo_exchange",
+    "rs_comm_unique_id", "rs_comm_init", "rs_comm_destroy", "rs_allgather",
 )
 
 _lib = None
@@ -89,6 +90,14 @@ def lib():
             L.rs_device_attribute.argtypes = [i, ctypes.POINTER(i)]
             L.rs_device_count.argtypes = [ctypes.POINTER(i)]
             L.rs_nvrtc_version.argtypes = [ctypes.POINTER(i), ctypes.POINTER(i)]
+            L.rs_ipc_handle.argtypes = [vp, ctypes.POINTER(sz), vp]
+            L.rs_ipc_open.argtypes = [ctypes.POINTER(vp), vp, sz]
+            L.rs_ipc_close.argtypes = [vp]
+            L.rs_halo_exchange.argtypes = [vp, sz, sz, vp, sz, vp, vp]
+            L.rs_comm_unique_id.argtypes = [vp]
+            L.rs_comm_init.argtypes = [ctypes.POINTER(vp), i, i, vp]
+            L.rs_comm_destroy.argtypes = [vp]
+            L.rs_allgather.argtypes = [vp, vp, vp, sz, vp]
             _lib = L
     return _lib
 
@@ -357,3 +366,57 @@ def tma_desc_2d_f32(base_ptr, dim0, dim1, row_stride_bytes, box0, box1, swizzle=
 class TensorMap(ctypes.Structure):
     _pack_ = 64
     _fields_ = [("words", ctypes.c_uint64 * 16)]
+
+
+# multi-GPU: peer memory and NCCL (include/rise_b200.h "multi-GPU") ---------
+
+
+def ipc_handle(dptr):
+    """(64-byte handle, offset) exporting the allocation that holds dptr."""
+    init()
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_size_t()
+    check_run(lib().rs_ipc_handle(h, ctypes.byref(off), _vp(dptr)), "rs_ipc_handle")
+    return h.raw, int(off.value)
+
+
+def ipc_open(handle: bytes, offset: int) -> int:
+    init()
+    out = ctypes.c_void_p()
+    check_run(lib().rs_ipc_open(ctypes.byref(out), ctypes.create_string_buffer(handle, 64), offset), "rs_ipc_open")
+    return int(out.value)
+
+
+def ipc_close(dptr):
+    check_run(lib().rs_ipc_close(_vp(dptr)), "rs_ipc_close")
+
+
+def halo_exchange(band_ptr, row_bytes, rows, above=None, above_rows=0, below=None, stream=None):
+    check_run(lib().rs_halo_exchange(_vp(band_ptr), row_bytes, rows, _vp(above or 0), above_rows,
+                                     _vp(below or 0), _stream_ptr(stream)), "rs_halo_exchange")
+
+
+def comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check_run(lib().rs_comm_unique_id(buf), "rs_comm_unique_id")
+    return buf.raw
+
+
+class NcclComm:
+    """An NCCL communicator owned by the native runtime."""
+
+    def __init__(self, nranks: int, rank: int, unique_id: bytes):
+        init()
+        self.h = ctypes.c_void_p()
+        self.nranks, self.rank = nranks, rank
+        check_run(lib().rs_comm_init(ctypes.byref(self.h), nranks, rank, ctypes.create_string_buffer(unique_id, 128)),
+                  "rs_comm_init")
+
+    def allgather(self, send_ptr, recv_ptr, bytes_per_rank, stream=None):
+        check_run(lib().rs_allgather(self.h, _vp(send_ptr), _vp(recv_ptr), bytes_per_rank, _stream_ptr(stream)),
+                  "rs_allgather")
+
+    def close(self):
+        if self.h:
+            check_run(lib().rs_comm_destroy(self.h), "rs_comm_destroy")
+            self.h = ctypes.c_void_p()

@@ -99,3 +99,75 @@ def sharded_nbody(step_fn, pos_block, vel_block, mass_block, group=None):
     all_pos = torch.cat(allgather_rank_order(pos_block, group), dim=0)
     all_mass = torch.cat(allgather_rank_order(mass_block, group), dim=0)
     return step_fn(pos_block, vel_block, all_pos, all_mass)
+
+
+# ---------------------------------------------------------------------------
+# device data path through the native runtime (include/rise_b200.h
+# "multi-GPU"): torch.distributed only carries the opaque handles / ids.
+
+
+class PeerHalo:
+    """Halo rows of a row band pulled from the neighbours' bands through peer
+    memory (CUDA IPC mappings; NVLink between GPUs): rs_halo_exchange.
+
+    `band` is this rank's device tensor [rows + 2, m] (rows 1..rows owned).
+    The neighbours' bands are mapped once; `exchange()` enqueues the two row
+    copies (the global edges get the clamped own edge row, padClamp2D)."""
+
+    def __init__(self, band, group=None):
+        import torch.distributed as dist
+
+        from . import runtime
+
+        self.band = band
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.rows = band.shape[0] - 2
+        self.row_bytes = band.shape[1] * band.element_size()
+        handle, off = runtime.ipc_handle(band.data_ptr())
+        peers = [None] * self.world
+        dist.all_gather_object(peers, (handle, off, self.rows), group=group)
+        self.above = self.below = None
+        self.above_rows = 0
+        if self.rank > 0:
+            h, o, r = peers[self.rank - 1]
+            self.above, self.above_rows = runtime.ipc_open(h, o), r
+        if self.rank < self.world - 1:
+            h, o, _r = peers[self.rank + 1]
+            self.below = runtime.ipc_open(h, o)
+
+    def exchange(self, stream=None):
+        from . import runtime
+
+        runtime.halo_exchange(self.band.data_ptr(), self.row_bytes, self.rows, self.above, self.above_rows,
+                              self.below, stream)
+
+    def close(self):
+        from . import runtime
+
+        for p in (self.above, self.below):
+            if p:
+                runtime.ipc_close(p)
+        self.above = self.below = None
+
+
+class DeviceComm:
+    """An NCCL communicator of the native runtime over a torch.distributed
+    group (rank 0's ncclUniqueId is broadcast through the group)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        from . import runtime
+
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [runtime.comm_unique_id() if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        self.comm = runtime.NcclComm(self.world, self.rank, obj[0])
+
+    def allgather(self, send, recv, stream=None):
+        """recv (world * send.numel()) <- every rank's send, in rank order."""
+        assert recv.numel() == send.numel() * self.world
+        self.comm.allgather(send.data_ptr(), recv.data_ptr(), send.numel() * send.element_size(), stream)
+
+    def close(self):
+        self.comm.close()

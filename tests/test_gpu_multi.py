@@ -1,0 +1,127 @@
+"""Multi-process data path of the native runtime on ONE GPU (the round's GPU
+budget is one device): two ranks on cuda:0 exchange conv halo rows through
+peer memory (rs_ipc_* + rs_halo_exchange) and run the sharded conv through
+the sm100a stencil kernel; the NCCL communicator (rs_comm_*, rs_allgather)
+runs at world size 1 (NCCL rejects two ranks on one device).  Handles and
+ids travel over gloo (plumbing), the data never leaves the device."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+W3 = (np.array([[1, 2, 1], [2, 4, 2], [1, 2, 1]], np.float32) / 16).astype(np.float32)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _halo_worker(rank, world, port, n, m, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2201_03611_b200 import compile_program, emit_cuda, programs, shard
+        from paper_2201_03611_b200.run import Executable
+
+        torch.cuda.set_device(0)
+        img = oracle.rng_inputs(3, n, m)
+        r0, rows = shard.row_band(n, world, rank)
+        band = torch.zeros((rows + 2, m), dtype=torch.float32, device="cuda")
+        band[1:-1] = torch.from_numpy(img[r0:r0 + rows]).cuda()
+        torch.cuda.synchronize()
+        dist.barrier()  # every band is written before any neighbour pulls from it
+        halo = shard.PeerHalo(band)
+        halo.exchange()
+        torch.cuda.synchronize()
+        top = img[r0 - 1] if rank > 0 else img[0]
+        bot = img[r0 + rows] if rank < world - 1 else img[n - 1]
+        ok_halo = np.array_equal(band[0].cpu().numpy(), top) and np.array_equal(band[-1].cpu().numpy(), bot)
+        # the unchanged conv program on the (rows + 2)-row local image, middle rows kept
+        c = compile_program(programs.CONV, None, name="conv")
+        exe = Executable(emit_cuda(c.unit), {"n": rows + 2, "m": m})
+        w = torch.from_numpy(W3.reshape(-1)).cuda()
+        out = torch.empty((rows + 2) * m, dtype=torch.float32, device="cuda")
+        exe(band.reshape(-1), w, out=out)
+        torch.cuda.synchronize()
+        got = out.view(rows + 2, m)[1:-1].cpu().numpy()
+        ok_conv = np.array_equal(got, oracle.conv3x3(img, W3)[r0:r0 + rows])
+        kinds = exe.template_kinds
+        dist.barrier()  # neighbours are done reading this band
+        halo.close()
+        q.put((rank, ok_halo, ok_conv, kinds))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,m", [(2, 256, 512), (3, 130, 260)])
+def test_peer_halo_sharded_conv_bit_exact(world, n, m):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, n, m, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok_halo, ok_conv, kinds in res:
+        assert ok_halo, f"rank {rank}: halo rows differ"
+        assert ok_conv, f"rank {rank}: sharded conv differs from the oracle"
+        assert kinds == ["stencil2d"]
+
+
+def _comm_worker(port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        from paper_2201_03611_b200 import shard
+
+        torch.cuda.set_device(0)
+        comm = shard.DeviceComm()
+        send = torch.arange(1000, dtype=torch.float32, device="cuda")
+        recv = torch.zeros(1000, dtype=torch.float32, device="cuda")
+        comm.allgather(send, recv)
+        torch.cuda.synchronize()
+        ok = bool(torch.equal(send, recv))
+        comm.close()
+        q.put(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_allgather_world_one():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_comm_worker, args=(_free_port(), q))
+    p.start()
+    ok = q.get(timeout=240)
+    p.join(timeout=60)
+    assert p.exitcode == 0 and ok
+
+
+def test_halo_exchange_clamps_at_global_edges(gpu):
+    from paper_2201_03611_b200 import runtime
+
+    m, rows = 64, 5
+    band = torch.zeros((rows + 2, m), dtype=torch.float32, device="cuda")
+    band[1:-1] = torch.arange(rows * m, dtype=torch.float32, device="cuda").view(rows, m)
+    runtime.halo_exchange(band.data_ptr(), m * 4, rows)
+    torch.cuda.synchronize()
+    assert torch.equal(band[0], band[1]) and torch.equal(band[-1], band[-2])

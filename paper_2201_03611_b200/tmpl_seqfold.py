@@ -8,11 +8,12 @@ Matches a serial stage of the form
 
 (the second stage of the chunked dot, or any `reduceSeq` emitted with
 reassociate=False).  The dependent chain of K adds cannot be parallelised
-without reordering, so the template makes the chain the only cost: one warp
-stages 1024-element tiles of every stream into a double-buffered shared
-memory ring with coalesced 128-bit loads (the next tile is in flight while
-the current one is folded), and lane 0 runs the program's own step
-expression over shared memory.  Order: PRESERVED (bit-exact).
+without reordering, so the template makes the chain the only cost: one lane
+streams 2048-element tiles of every stream into a 3-stage shared-memory ring
+with 1-D bulk copies (TMA; the next tiles are in flight while the current
+one is folded, and the lane never waits on a global load) and runs the
+program's own step expression over float4 reads of shared memory, so the
+chain advances at the FADD latency.  Order: PRESERVED (bit-exact).
 """
 
 from __future__ import annotations
@@ -21,7 +22,8 @@ from . import lir
 from ._ref import nat
 from .emit_cuda import NatRenderer, ValueRenderer, kernel_head, py_expr
 
-TILE = 1024
+TILE = 2048  # floats per stage (split among the streams: static smem stays < 48 KB)
+STAGES = 3
 
 
 def match(prog, stage, base_name, temps, exact, fold_shape, j_coefficient, thread_lines):
@@ -56,53 +58,76 @@ def match(prog, stage, base_name, temps, exact, fold_shape, j_coefficient, threa
     name = f"{base_name}_seqfold"
     ns = len(s_list)
 
-    def hook(ld):
-        if ld in streams:
-            return f"rs_st[{s_list.index(streams[ld])} * {TILE} + rs_jj]"
-        return None
+    def step_with(comp):
+        def hook(ld):
+            if ld in streams:
+                return f"rs_v{s_list.index(streams[ld])}.{comp}" if comp else \
+                    f"rs_ring[rs_q][{s_list.index(streams[ld])}][rs_jj]"
+            return None
 
-    vstep = ValueRenderer(prog, exact, load_hook=hook)(step)
+        return ValueRenderer(prog, exact, load_hook=hook)(step)
+
+    pre = [f"({py_expr(base)}) % 4 == 0" for _b, base in s_list]
     lines = kernel_head(prog, name, temps, launch_bounds=32)
     lines += [
         f"  constexpr int RS_K = {r(loop.bound)};",
-        f"  __shared__ __align__(16) float rs_ring[2][{ns} * {TILE}];",
+        f"  constexpr int RS_TILE = {max(256, TILE // ns)}, RS_S = {STAGES}, RS_NS = {ns};",
+        "  constexpr int RS_NT = (RS_K + RS_TILE - 1) / RS_TILE;",
+        "  __shared__ __align__(128) float rs_ring[RS_S][RS_NS][RS_TILE];",
+        "  __shared__ __align__(8) unsigned long long rs_bar[RS_S];",
     ]
     for k, (buf, base) in enumerate(s_list):
         lines.append(f"  const float* rs_g{k} = {buf} + ({r(base)});")
     lines += [
-        "  const int rs_lane = threadIdx.x;",
-        "  auto rs_stage = [&](int rs_t, float* rs_dst) {",
-        f"    const int rs_j0 = rs_t * {TILE};",
-        f"    for (int rs_e = rs_lane; rs_e < {TILE}; rs_e += 32) {{",
-        "      const int rs_j = rs_j0 + rs_e;",
+        "  if (threadIdx.x != 0) return;  // the fold is one dependent chain: one lane runs it",
+        "  for (int rs_q = 0; rs_q < RS_S; ++rs_q) rs_mbar_init(&rs_bar[rs_q], 1);",
+        "  rs_fence_barrier_init();",
+        "  // tile t -> stage t % S by 1-D bulk copies (TMA); the tail of K % 4 elements is read directly",
+        "  constexpr int RS_K4 = RS_K / 4 * 4;",
+        "  auto rs_issue = [&](int rs_t) {",
+        "    const int rs_j0 = rs_t * RS_TILE;",
+        "    const int rs_n4 = RS_K4 - rs_j0 < RS_TILE ? RS_K4 - rs_j0 : RS_TILE;",
+        "    if (rs_n4 <= 0) return;",
+        "    const int rs_q = rs_t % RS_S;",
+        "    rs_mbar_arrive_expect_tx(&rs_bar[rs_q], (unsigned)(rs_n4 * 4 * RS_NS));",
     ]
     for k in range(ns):
-        lines.append(f"      rs_dst[{k} * {TILE} + rs_e] = rs_j < RS_K ? __ldg(rs_g{k} + rs_j) : 0.0f;")
+        lines.append(f"    rs_bulk_g2s(rs_ring[rs_q][{k}], rs_g{k} + rs_j0, (unsigned)(rs_n4 * 4), &rs_bar[rs_q]);")
+    lines += [
+        "  };",
+        "  for (int rs_t = 0; rs_t < RS_S - 1 && rs_t < RS_NT; ++rs_t) rs_issue(rs_t);",
+        f"  {acc.ctype} {acc.name} = {ValueRenderer(prog, exact)(init.value)};",
+        "  for (int rs_t = 0; rs_t < RS_NT; ++rs_t) {",
+        "    if (rs_t + RS_S - 1 < RS_NT) {  // its stage was folded (generic-proxy reads) at t - 1",
+        "      rs_fence_proxy_async();",
+        "      rs_issue(rs_t + RS_S - 1);",
+        "    }",
+        "    const int rs_q = rs_t % RS_S;",
+        "    const int rs_j0 = rs_t * RS_TILE;",
+        "    const int rs_n4 = RS_K4 - rs_j0 < RS_TILE ? (RS_K4 - rs_j0 > 0 ? RS_K4 - rs_j0 : 0) : RS_TILE;",
+        "    if (rs_n4 > 0) rs_mbar_wait(&rs_bar[rs_q], (unsigned)((rs_t / RS_S) & 1));",
+        "#pragma unroll 4",
+        "    for (int rs_jj = 0; rs_jj < rs_n4; rs_jj += 4) {",
+    ]
+    for k in range(ns):
+        lines.append(f"      const float4 rs_v{k} = *reinterpret_cast<const float4*>(&rs_ring[rs_q][{k}][rs_jj]);")
+    for comp in ("x", "y", "z", "w"):
+        lines.append(f"      {acc.name} = {step_with(comp)};")
     lines += [
         "    }",
-        "  };",
-        f"  constexpr int RS_NT = (RS_K + {TILE - 1}) / {TILE};",
-        f"  {acc.ctype} {acc.name} = {ValueRenderer(prog, exact)(init.value)};",
-        "  if (RS_NT > 0) rs_stage(0, rs_ring[0]);",
-        "  __syncwarp();",
-        "  for (int rs_t = 0; rs_t < RS_NT; ++rs_t) {",
-        "    if (rs_t + 1 < RS_NT) rs_stage(rs_t + 1, rs_ring[(rs_t + 1) & 1]);  // next tile in flight",
-        "    if (rs_lane == 0) {",
-        "      const float* rs_st = rs_ring[rs_t & 1];",
-        f"      const int rs_n = RS_K - rs_t * {TILE} < {TILE} ? RS_K - rs_t * {TILE} : {TILE};",
-        "#pragma unroll 8",
-        "      for (int rs_jj = 0; rs_jj < rs_n; ++rs_jj) {",
-        f"        {acc.name} = {vstep};",
-        "      }",
-        "    }",
-        "    __syncwarp();",
         "  }",
-        "  if (rs_lane == 0) {",
+        "  for (int rs_j = RS_K4; rs_j < RS_K; ++rs_j) {  // K % 4 tail, straight from global memory",
     ]
-    for s in post:
-        lines += ["    " + x for x in thread_lines(prog, s, exact)]
-    lines += ["  }", "}"]
-    plan = {"name": name, "kind": "seqfold", "fmad": False, "order": "preserved", "pre": []}
+    for k in range(ns):
+        lines.append(f"    const float4 rs_v{k} = make_float4(rs_g{k}[rs_j], 0.0f, 0.0f, 0.0f);")
+    lines += [
+        f"    {acc.name} = {step_with('x')};",
+        "  }",
+    ]
+    for s_ in post:
+        lines += ["  " + x for x in thread_lines(prog, s_, exact)]
+    lines += ["}"]
+    plan = {"name": name, "kind": "seqfold", "fmad": False, "order": "preserved", "pre": pre}
     return "\n".join(lines) + "\n", plan
 
 

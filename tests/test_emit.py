@@ -49,6 +49,23 @@ def test_templates_compile_for_sm100a_with_nvrtc(key):
     assert cubin[:4] == b"\x7fELF" and len(lowered) == len(names)
 
 
+@pytest.mark.parametrize("source,strategy,name,assume,nats", [
+    (programs.DOT, programs.DOT_STRATEGY, "dot", False, {"n": 65536}),
+    (programs.DOT_CHUNKED, None, "dotChunked", True, {"n": 1 << 24}),
+    (programs.MV, programs.MV_GLOBAL_STRATEGY, "mv", False, {"n": 256, "m": 512}),
+], ids=["dot", "dot_chunked", "mv"])
+def test_order_preserving_emission_compiles_for_sm100a(source, strategy, name, assume, nats):
+    """reassociate=False kernels (seqfold, rowfold, generic) through NVRTC +
+    ptxas: catches resource overflows (e.g. static shared memory) on CPU."""
+    assumptions = [(nat.Var("n"), nat.Const(programs.DOT_CHUNK))] if assume else None
+    c = compile_program(source, strategy, name=name, **({"assumptions": assumptions} if assumptions else {}))
+    code = emit_cuda(c.unit, reassociate=False)
+    targs = ", ".join(str(nats[p]) for p in code.plan["nat_params"])
+    names = [f"{s['name']}<{targs}>" for st in code.plan["stages"] for s in (st, st.get("fallback")) if s]
+    cubin, lowered = runtime.compile_cubin(code.text, names, ["--fmad=false"])
+    assert cubin[:4] == b"\x7fELF" and len(lowered) == len(names)
+
+
 def test_emit_keeps_reference_targets_and_rejects_cuda():
     c = programs.compile_config("gemv")
     assert emit(c.unit, "openmp") == codegen.emit(c.unit, "openmp")

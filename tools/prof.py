@@ -27,7 +27,7 @@ def main():
 
     wl = bench.WORKLOADS[args.workload]()
     compiled, nats = wl.compile()
-    exe = Executable(emit_cuda(compiled.unit), nats)
+    exe = Executable(emit_cuda(compiled.unit, **wl.emit_kwargs), nats)
     dev = [torch.from_numpy(h.reshape(-1)).to("cuda") for h in wl.inputs()]
     out = torch.empty(exe.output_size, dtype=torch.float32, device="cuda")
     for _ in range(args.iters):

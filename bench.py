@@ -175,9 +175,15 @@ class Conv(Workload):
 
         img, w = host
         rows = 1024
-        t = _best_of(lambda: oracle.conv3x3(img[:rows], w), 3)
+        if oracle.ref_lib() is not None:
+            t = _best_of(lambda: oracle.ref_conv3x3(img[:rows], w), 3)
+            kind, what = "reference", ("the reference's emitted OpenMP C for programs.CONV (extension "
+                                       "primitives through the emitter's seams, oracle/_ref)")
+        else:
+            t = _best_of(lambda: oracle.conv3x3(img[:rows], w), 3)
+            kind, what = "port", "C restatement (oracle/rise_oracle.c), OpenMP"
         return {"value": 4.0 * 2 * rows * self.m / t / 1e9, "unit": "GB/s", "cores": oracle.threads(),
-                "kind": "port", "sample": f"{rows}x{self.m} band, C restatement (oracle/rise_oracle.c), OpenMP"}
+                "kind": kind, "sample": f"{rows}x{self.m} band, {what}"}
 
 
 class Sgemm(Workload):
@@ -241,9 +247,15 @@ class Nbody(Workload):
 
         pos, vel, mass = host
         count = 256
-        t = _best_of(lambda: oracle.nbody(pos, vel, mass, 0, count), 2)
+        if oracle.ref_lib() is not None:
+            t = _best_of(lambda: oracle.ref_nbody_block(pos, vel, mass, 0, count), 2)
+            kind, what = "reference", ("the reference's emitted OpenMP C for programs.NBODY_SHARD (extension "
+                                       "primitives through the emitter's seams, oracle/_ref)")
+        else:
+            t = _best_of(lambda: oracle.nbody(pos, vel, mass, 0, count), 2)
+            kind, what = "port", "C restatement, OpenMP"
         return {"value": 20.0 * count * self.n / t / 1e9, "unit": "GFLOP/s", "cores": oracle.threads(),
-                "kind": "port", "sample": f"{count} target bodies x {self.n} sources, C restatement, OpenMP"}
+                "kind": kind, "sample": f"{count} target bodies x {self.n} sources, {what}"}
 
 
 WORKLOADS = {w.key: w for w in (Gemv, GemvOpt, Dot, DotChunked, Conv, Sgemm, Nbody)}

@@ -69,6 +69,8 @@ def ref_lib():
         L.mvKernel.argtypes = [_fp, _int, _int, _fp, _fp]
         L.mvOptKernel.argtypes = [_fp, _int, _int, _int, _fp, _fp]
         L.sgemmBtKernel.argtypes = [_fp, _int, _int, _int, _fp, _fp]
+        L.convKernel.argtypes = [_fp, _int, _int, _fp, _fp]
+        L.nbodyShardKernel.argtypes = [_fp, _int, _int, _fp, _fp, _fp, _fp]
         _ref = L
     return _ref
 
@@ -169,6 +171,29 @@ def ref_mv(M, x, s=None):
         L.mvKernel(_ptr(out), n, m, _ptr(M), _ptr(x))
     else:
         L.mvOptKernel(_ptr(out), n, m, s, _ptr(M), _ptr(x))
+    return out
+
+
+def ref_conv3x3(img, w):
+    """The reference emitter's OpenMP C for programs.CONV (extension seams)."""
+    L = ref_lib()
+    img, w = f32(img), f32(w)
+    n, m = img.shape
+    out = np.zeros((n, m), np.float32)
+    L.convKernel(_ptr(out), n, m, _ptr(img), _ptr(w))
+    return out
+
+
+def ref_nbody_block(pos, vel, mass, first, count):
+    """The reference emitter's OpenMP C for programs.NBODY_SHARD: the step of
+    target bodies first .. first+count-1 against all sources."""
+    L = ref_lib()
+    pos, vel, mass = f32(pos), f32(vel), f32(mass)
+    n = mass.size
+    tpos = np.ascontiguousarray(pos[first:first + count])
+    tvel = np.ascontiguousarray(vel[first:first + count])
+    out = np.zeros((count, 3), np.float32)
+    L.nbodyShardKernel(_ptr(out), count, n, _ptr(tpos), _ptr(tvel), _ptr(pos), _ptr(mass))
     return out
 
 

@@ -13,6 +13,12 @@ spellings.  Each is added in four places, and nowhere else:
 4. oracle    — `interpreter._PRIM_ARITY` + `_exec_prim` (interpreter.py:58-185)
                for `eval_program`, and `_eval_fun_prim` / `eval_acc_phrase`
                (interpreter.py:491-564) for `run_unit`.
+5. C emitter — `codegen.emit_exp` / `emit_acc` (codegen.py:179-290, module
+               functions that recurse through their globals, so a wrapper
+               sees every level) and `codegen.emit` (helpers), so the
+               reference's own C / OpenMP emission covers the programs that
+               use them (the CPU baseline and full-size oracle of conv and
+               nbody, oracle/make_ref.py).
 
 Semantics (there is no reference oracle for these — "parity unpinned" for
 them in the sense of SURVEY.md §8 c; these definitions are the spec):
@@ -36,7 +42,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from ._ref import dpia, errors, interpreter, lowering, nat, primitives
+from ._ref import codegen, dpia, errors, interpreter, lowering, nat, primitives
 from .types_util import array_elem
 
 # ---------------------------------------------------------------------------
@@ -97,6 +103,7 @@ def install(registry=None):
         dpia.SIGNATURES[tag] = dpia._parse_signature(tag, text)
     _install_lowering()
     _install_interpreter()
+    _install_c_emitter()
     _installed = True
     return registry
 
@@ -304,6 +311,85 @@ def _install_interpreter():
         return base_acc(p, env, store, nat_env)
 
     interpreter.eval_acc_phrase = eval_acc_phrase
+
+
+# ---------------------------------------------------------------------------
+# 5. C emission (the reference's C / OpenMP targets)
+
+C_HELPERS = """static inline int rs_clamp(int k, int hi) { return k < 0 ? 0 : (k > hi ? hi : k); }
+"""
+
+
+def _clamp_nat(k, hi, state):
+    """A clamped index as a nat atom: nat.py has no min/max node (SURVEY.md
+    §8.1), so the clamp is an opaque variable whose name IS its C text
+    (codegen._render prints a Var's name verbatim); normalisation keeps it as
+    an atom, and equal clamps share one atom."""
+    inner = codegen._render_nat(k, state)
+    return nat.Var(f"rs_clamp({inner}, {codegen._render_nat(nat.normalize(hi - nat.Const(1)), state)})")
+
+
+def _install_c_emitter():
+    base_exp = codegen.emit_exp
+    base_acc = codegen.emit_acc
+    base_emit = codegen.emit
+
+    def emit_exp(p, env, state, pending=(), projs=()):
+        if isinstance(p, dpia.FunPrim) and p.tag in VIEW_TAGS:
+            x = p.args[0]
+            ta = p.type_args
+            if p.tag == "transpose":
+                i, j, *rest = pending
+                return emit_exp(x, env, state, (j, i, *rest), projs)
+            if p.tag == "slide":
+                sp = ta[1]
+                i, a, *rest = pending
+                return emit_exp(x, env, state, (i * sp + a, *rest), projs)
+            if p.tag == "slide2D":
+                sp = ta[1]
+                i, j, a, b, *rest = pending
+                return emit_exp(x, env, state, (i * sp + a, j * sp + b, *rest), projs)
+            if p.tag == "padClamp":
+                l, _r, n = ta[0], ta[1], ta[2]
+                k, *rest = pending
+                return emit_exp(x, env, state, (_clamp_nat(k - l, n, state), *rest), projs)
+            if p.tag == "padClamp2D":
+                l, _r, n, m = ta[0], ta[1], ta[2], ta[3]
+                i, j, *rest = pending
+                return emit_exp(x, env, state, (_clamp_nat(i - l, n, state), _clamp_nat(j - l, m, state), *rest),
+                                projs)
+        if isinstance(p, dpia.FunPrim) and p.tag in BINARY_TAGS + UNARY_TAGS:
+            if pending or projs:
+                raise errors.EmitError("indexed arithmetic value")
+            a = emit_exp(p.args[0], env, state)
+            if p.tag == "div":
+                return f"({a} / {emit_exp(p.args[1], env, state)})"
+            if p.tag == "sqrt":
+                return f"sqrtf({a})"
+            return f"(1.0f / sqrtf({a}))"  # rsqrt: both operations rounded to binary32
+        return base_exp(p, env, state, pending, projs)
+
+    def emit_acc(p, env, state, pending=()):
+        if isinstance(p, dpia.ImpPrim) and p.tag == "transposeAcc":
+            i, j, *rest = pending
+            return emit_acc(p.args[0], env, state, (j, i, *rest))
+        return base_acc(p, env, state, pending)
+
+    def emit(unit, target):
+        text = base_emit(unit, target)
+        if target != "opencl":
+            head = []
+            if "sqrtf(" in text:
+                head.append("#include <math.h>")
+            if "rs_clamp(" in text:
+                head.append(C_HELPERS.rstrip())
+            if head:
+                text = "\n".join(head) + "\n" + text
+        return text
+
+    codegen.emit_exp = emit_exp
+    codegen.emit_acc = emit_acc
+    codegen.emit = emit
 
 
 def ensure_installed():

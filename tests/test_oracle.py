@@ -91,6 +91,32 @@ def test_restatement_equals_reference_c_at_size():
     np.testing.assert_array_equal(oracle.sgemm_bt(A, Bt), oracle.ref_sgemm_bt(A, Bt))
 
 
+@needs_ref
+def test_reference_emitted_c_of_extension_programs_matches_golden():
+    """conv / nbody through the reference's own emitter with the extension's
+    emit_exp cases (extension.py §5) == the extension interpreter's golden
+    vectors, bit for bit."""
+    (img, w), out, _ = _case("conv")
+    np.testing.assert_array_equal(oracle.ref_conv3x3(img, w).view(np.uint32), out.view(np.uint32))
+    (pos, vel, mass), out, _ = _case("nbody")
+    n = mass.size
+    got = oracle.ref_nbody_block(pos, vel, mass, 0, n)
+    np.testing.assert_array_equal(got.view(np.uint32), out.reshape(n, 3).view(np.uint32))
+
+
+@needs_ref
+def test_restatement_equals_reference_c_of_extension_programs_at_size():
+    img = oracle.rng_inputs(3, 300, 260)
+    w = oracle.rng_inputs(7, 3, 3)
+    np.testing.assert_array_equal(oracle.conv3x3(img, w), oracle.ref_conv3x3(img, w))
+    n = 2048
+    pos = oracle.rng_inputs(5, n, 3)
+    vel = oracle.rng_inputs(6, n, 3, low=-0.1, high=0.1)
+    mass = oracle.rng_inputs(8, n, low=0.5, high=1.5)
+    np.testing.assert_array_equal(oracle.nbody(pos, vel, mass, 100, 64),
+                                  oracle.ref_nbody_block(pos, vel, mass, 100, 64))
+
+
 def test_left_fold_order_is_pinned():
     # interpreter.py:134-138: reduce is a left fold from init; 0.1+0.2+0.3 in
     # fp32 (test_interpreter.py:79-84) — the restatement does the same

@@ -275,12 +275,14 @@ RS_DEVICE void mbar_wait_cluster(unsigned long long* bar, unsigned phase) {
   }
 }
 
-template <unsigned IDESC>
-RS_DEVICE void mma2(unsigned tmem_d, unsigned long long adesc, unsigned long long bdesc, unsigned accumulate) {
+// the instruction descriptor is a register operand: one kernel issues both
+// full (N = BN) and half-width (N = BN / 2) tiles
+RS_DEVICE void mma2(unsigned tmem_d, unsigned long long adesc, unsigned long long bdesc, unsigned idesc,
+                    unsigned accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
 RS_DEVICE void commit2_multicast(unsigned long long* bar) {
@@ -315,11 +317,23 @@ struct Cfg2 {
   static constexpr unsigned TMEM_COLS = BN;
   static constexpr unsigned IDESC =
       (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(256 >> 4) << 24);
+  static constexpr unsigned IDESC_HALF =
+      (1u << 4) | (2u << 7) | (2u << 10) | (unsigned((BN / 2) >> 3) << 17) | (unsigned(256 >> 4) << 24);
 };
 
-// blockIdx.x = 2 * pair + rank; pair -> (tm, tn) with tn fastest
+// blockIdx.x = 2 * pair + rank.  Tiles 256 x BN in (tm, tn) order, tn
+// fastest.  Pairs below n_full each compute one whole tile.  The tiles after
+// them (the tail that would leave most SM pairs idle in a last partial wave:
+// 256 tiles on 74 pairs are 3.46 waves) are split along K: pair n_full + 2u
+// folds the first half of tile n_full + u's K loop, pair n_full + 2u + 1 the
+// second half, which it parks in `ws`; the first-half pair waits for it
+// (flag, release / acquire) and stores C = first + second.  Every split unit
+// is resident at once (the split is only used when the units fit in one
+// wave), the second half never waits, and the order of the final add is
+// fixed: deterministic.
 template <int M, int N, int K, int BN, int STAGES>
-RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* mapA, const rs_tmap* mapB) {
+RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* mapA, const rs_tmap* mapB,
+                               int n_full, float* __restrict__ ws, unsigned* __restrict__ flags) {
   using G = Cfg2<BN, STAGES>;
   extern __shared__ __align__(1024) unsigned char rs_gemm_smem_raw[];
   unsigned char* smem =
@@ -335,7 +349,13 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
   constexpr int NTN = N / BN;
   const unsigned rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1;
-  const int m0 = (pair / NTN) * 256, n0 = (pair % NTN) * BN;
+  const bool split = pair >= n_full;
+  const int unit = pair - n_full;  // split units only
+  const int tile = split ? n_full + (unit >> 1) : pair;
+  const int khalf = split ? (unit & 1) : 0;
+  const int kb0 = split && khalf ? KB / 2 : 0;
+  const int kb1 = split && !khalf ? KB / 2 : KB;
+  const int m0 = (tile / NTN) * 256, n0 = (tile % NTN) * BN;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto a_raw = [&](int s) { return smem + s * G::STAGE_BYTES; };
   auto a_lo = [&](int s) { return smem + s * G::STAGE_BYTES + G::TILE_A; };
@@ -361,9 +381,9 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < KB; ++kb) {
-        const int s = kb % STAGES;
-        const unsigned ph = (unsigned)((kb / STAGES) & 1);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const int s = (kb - kb0) % STAGES;
+        const unsigned ph = (unsigned)(((kb - kb0) / STAGES) & 1);
         rs_mbar_wait(&empty[s], ph ^ 1u);
         rs_mbar_arrive_expect_tx(&full[s], G::TILE_A + G::TILE_B);
         rs_tma_load_2d(a_raw(s), mapA, kb * BK, m0 + 128 * (int)rank, &full[s]);
@@ -372,9 +392,9 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
     }
   } else if (warp == 1) {
     if (rank == 0 && lane == 0) {
-      for (int kb = 0; kb < KB; ++kb) {
-        const int s = kb % STAGES;
-        const unsigned ph = (unsigned)((kb / STAGES) & 1);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const int s = (kb - kb0) % STAGES;
+        const unsigned ph = (unsigned)(((kb - kb0) / STAGES) & 1);
         mbar_wait_cluster(&conv[s], ph);
         fence_after();
         const unsigned long long ahi = smem_desc(rs_smem_addr(a_raw(s)));
@@ -384,9 +404,9 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
 #pragma unroll
         for (int k = 0; k < BK / 8; ++k) {
           const unsigned long long off = (unsigned long long)(k * 32) >> 4;
-          mma2<G::IDESC>(tmem, alo + off, bhi + off, (kb | k) != 0);
-          mma2<G::IDESC>(tmem, ahi + off, blo + off, 1u);
-          mma2<G::IDESC>(tmem, ahi + off, bhi + off, 1u);
+          mma2(tmem, alo + off, bhi + off, G::IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
+          mma2(tmem, ahi + off, blo + off, G::IDESC, 1u);
+          mma2(tmem, ahi + off, bhi + off, G::IDESC, 1u);
         }
         commit2_multicast(&empty[s]);
       }
@@ -395,9 +415,9 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
     __syncwarp();
   } else {
     const int t = threadIdx.x - 64;
-    for (int kb = 0; kb < KB; ++kb) {
-      const int s = kb % STAGES;
-      const unsigned ph = (unsigned)((kb / STAGES) & 1);
+    for (int kb = kb0; kb < kb1; ++kb) {
+      const int s = (kb - kb0) % STAGES;
+      const unsigned ph = (unsigned)(((kb - kb0) / STAGES) & 1);
       rs_mbar_wait(&full[s], ph);
       split_tile<false>(a_raw(s), a_lo(s), G::TILE_A, t);
       split_tile<false>(b_raw(s), b_lo(s), G::TILE_B, t);
@@ -410,16 +430,55 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
     fence_after();
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    float* crow = C + (long long)(m0 + 128 * (int)rank + row) * ldc + n0;
+    const int trow = 128 * (int)rank + row;  // row within the 256-row pair tile
+    float* crow = C + (long long)(m0 + trow) * ldc + n0;
+    // split tiles: this CTA's half of the parked second-K-half tile and its flag
+    float* wrow = ws + ((long long)(unit >> 1) * 256 + trow) * BN;
+    unsigned* flag = flags + 2 * (unit >> 1) + rank;
+    if (split && khalf == 0) {
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+      } while (v == 0u);
+    }
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
       unsigned r[32];
       tmem_ld32(tmem + ((unsigned)(q * 32) << 16) + (unsigned)c0, r);
+      if (!split) {
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        *reinterpret_cast<float4*>(crow + c0 + j) =
-            make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                        __uint_as_float(r[j + 3]));
+        for (int j = 0; j < 32; j += 4) {
+          *reinterpret_cast<float4*>(crow + c0 + j) =
+              make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                          __uint_as_float(r[j + 3]));
+        }
+      } else if (khalf == 1) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          __stcg(reinterpret_cast<float4*>(wrow + c0 + j),
+                 make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                             __uint_as_float(r[j + 3])));
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const float4 w = __ldcg(reinterpret_cast<const float4*>(wrow + c0 + j));
+          *reinterpret_cast<float4*>(crow + c0 + j) =
+              make_float4(__fadd_rn(__uint_as_float(r[j]), w.x), __fadd_rn(__uint_as_float(r[j + 1]), w.y),
+                          __fadd_rn(__uint_as_float(r[j + 2]), w.z), __fadd_rn(__uint_as_float(r[j + 3]), w.w));
+        }
+      }
+    }
+    if (split) {
+      // every epilogue thread of this CTA is done with the parked tile
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (t == 0) {
+        if (khalf == 1) {
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");  // the parked tile before the flag
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(1u) : "memory");
+        } else {
+          *flag = 0u;  // consumed: ready for the next launch
+        }
       }
     }
   }

@@ -191,6 +191,11 @@ class Executable:
             pitch = eval_py(extra.get("pitch", extra["dims"][0]), self.nats)
             return rt.tma_desc_2d_f32(base, dims[0], dims[1], pitch * 4, extra["box"][0], extra["box"][1],
                                       extra.get("swizzle", 0))
+        if kind == "gemm_full_tiles":
+            from .tmpl_gemm import full_tiles
+
+            return ctypes.c_int(full_tiles(eval_py(extra["M"], self.nats), eval_py(extra["N"], self.nats),
+                                           eval_py(extra["K"], self.nats), extra["bn"], self.sm_count))
         raise InterpreterError(f"unknown extra kernel argument {kind!r}")
 
     def run_host(self, host_inputs, host_out, device_inputs, device_out, stream=None):

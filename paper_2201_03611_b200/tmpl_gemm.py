@@ -76,11 +76,13 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
     r = NatRenderer(prog.clamps)
     bn, stages, write_hi = BN, STAGES, WRITE_HI
     extra = ["const __grid_constant__ rs_tmap rs_mapA", "const __grid_constant__ rs_tmap rs_mapB"]
+    if PAIR:
+        extra += ["int rs_nfull", "float* __restrict__ rs_ws", "unsigned* __restrict__ rs_flags"]
     lines = kernel_head(prog, name, temps, launch_bounds="192, 1", extra_params=extra)
     if PAIR:
         lines += [
             f"  rise_gemm::gemm_3xtf32_2sm<{r(M)}, {r(N)}, {r(K)}, {PAIR_BN}, {PAIR_STAGES}>"
-            f"({st.target.buf}, {r(N)}, &rs_mapA, &rs_mapB);",
+            f"({st.target.buf}, {r(N)}, &rs_mapA, &rs_mapB, rs_nfull, rs_ws, rs_flags);",
             "}",
         ]
         plan = {
@@ -88,10 +90,11 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
             "kind": "gemm_tc",
             "M": py_expr(M),
             "N": py_expr(N),
+            "K": py_expr(K),
             "bn": PAIR_BN,
             "pair": True,
             "fmad": False,
-            "order": "3xtf32 tensor-core, CTA pairs (reassociated)",
+            "order": "3xtf32 tensor-core, CTA pairs; tail tiles K-split in two halves (reassociated)",
             "pre": [f"({py_expr(M)}) % 256 == 0", f"({py_expr(N)}) % {PAIR_BN} == 0", f"({py_expr(K)}) % 32 == 0",
                     f"({py_expr(M)}) * ({py_expr(N)}) * ({py_expr(K)}) > 0"],
             "smem": PAIR_STAGES * 2 * (128 * 32 * 4 + (PAIR_BN // 2) * 32 * 4) + 1024 + 256,
@@ -100,7 +103,13 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
                  "pitch": py_expr(K), "box": [32, 128], "swizzle": 3},
                 {"kind": "tma2d", "buf": b_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(N)],
                  "pitch": py_expr(K), "box": [32, PAIR_BN // 2], "swizzle": 3},
+                {"kind": "gemm_full_tiles", "M": py_expr(M), "N": py_expr(N), "K": py_expr(K), "bn": PAIR_BN},
+                {"kind": "workspace", "name": f"rs_ws_{base_name}_ktail"},
+                {"kind": "workspace", "name": f"rs_ws_{base_name}_kflags"},
             ],
+            # K-split tail tiles park their second halves here (<= one wave of pair tiles)
+            "workspace": [{"name": f"rs_ws_{base_name}_ktail", "ctype": "float", "size": f"74 * 256 * {PAIR_BN}"},
+                          {"name": f"rs_ws_{base_name}_kflags", "ctype": "int", "size": "2 * 74"}],
         }
         return "\n".join(lines) + "\n", plan
     lines += [
@@ -129,11 +138,32 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
     return "\n".join(lines) + "\n", plan
 
 
+SPLIT_SLOTS_MAX = 74  # workspace sizing: at most this many split tiles (one wave of B200 SM pairs)
+
+
+def full_tiles(M, N, K, bn, sm):
+    """How many 256 x bn pair tiles run whole.  The tail past the last whole
+    wave of SM pairs is split along K into two units per tile when those
+    units fit in one wave (else nothing is split).  RISE_GEMM_KSPLIT=0
+    disables the split."""
+    tiles = (M // 256) * (N // bn)
+    slots = max(1, sm // 2)
+    tail = tiles % slots
+    if (os.environ.get("RISE_GEMM_KSPLIT", "1") != "1" or tail == 0 or tiles < slots or 2 * tail > slots
+            or tail > SPLIT_SLOTS_MAX or K // 32 < 2):
+        return tiles
+    return tiles - tail
+
+
 def launch(st, nats, sm):
     from .emit_cuda import eval_py
 
     M = eval_py(st["M"], nats)
     N = eval_py(st["N"], nats)
     if st.get("pair"):
-        return (2 * (M // 256) * (N // st["bn"]), 1, 1), (192, 1, 1), st["smem"], (2, 1, 1)
+        K = eval_py(st["K"], nats)
+        tiles = (M // 256) * (N // st["bn"])
+        nfull = full_tiles(M, N, K, st["bn"], sm)
+        pairs = nfull + 2 * (tiles - nfull)
+        return (2 * pairs, 1, 1), (192, 1, 1), st["smem"], (2, 1, 1)
     return (N // st["bn"], M // 128, 1), (192, 1, 1), st["smem"], (1, 1, 1)

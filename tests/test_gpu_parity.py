@@ -4,6 +4,7 @@ Bit-exact where the kernel preserves the program's order (generic kernels,
 `rowfold`); fp64 error bound where a template reassociates (`reduce`)."""
 
 import numpy as np
+import torch
 import pytest
 
 import oracle
@@ -172,6 +173,42 @@ def test_sgemm_tcgen05_within_bound(gpu, n, m, k):
     assert np.all(err <= oracle.gemm_bound(k, absC)), float(np.max(err / (absC * oracle.U * k)))
     # 3xTF32 must be far more accurate than plain TF32 (~2^-11 relative)
     assert float(np.max(err / absC)) < 1e-5
+
+
+@pytest.mark.parametrize("n,m,k", [(2560, 2560, 256), (4096, 4096, 512)])
+def test_sgemm_k_split_tail_tiles(gpu, n, m, k, monkeypatch):
+    """Tiles past the last whole wave of SM pairs are split along K into two
+    units (tmpl_gemm.full_tiles) that meet through a workspace and a flag:
+    within the 3xTF32 bound, deterministic over repeated launches (the flags
+    reset themselves), and no further from fp64 than the unsplit launch."""
+    from paper_2201_03611_b200 import tmpl_gemm
+    from paper_2201_03611_b200.run import Executable
+
+    sm = gpu.device_attribute(16)
+    tiles = (n // 256) * (m // 256)
+    assert tmpl_gemm.full_tiles(n, m, k, 256, sm) < tiles  # the split really happens at this size
+    c = compile_program(programs.SGEMM_BT, None, name="sgemm")
+    code = emit_cuda(c.unit)
+    A = oracle.rng_inputs(4, n, k)
+    Bt = oracle.rng_inputs(14, m, k)
+    dA, dB = torch.from_numpy(A.reshape(-1)).cuda(), torch.from_numpy(Bt.reshape(-1)).cuda()
+    nats = {"n": n, "m": m, "k": k}
+    monkeypatch.setenv("RISE_GEMM_KSPLIT", "1")
+    exe = Executable(code, nats)
+    runs = [exe(dA, dB).cpu().numpy() for _ in range(3)]
+    for r in runs[1:]:
+        np.testing.assert_array_equal(r.view(np.uint32), runs[0].view(np.uint32))
+    monkeypatch.setenv("RISE_GEMM_KSPLIT", "0")
+    whole = Executable(code, nats)(dA, dB).cpu().numpy().reshape(n, m)
+    got = runs[0].reshape(n, m)
+    rows = slice(n - 256, n)  # the last row block holds split tiles
+    C64, absC = oracle.sgemm_bt_f64(A[rows], Bt)
+    err = np.abs(got[rows] - C64)
+    assert np.all(err <= oracle.gemm_bound(k, absC))
+    assert float(np.max(err / absC)) < 1e-5
+    assert float(np.max(np.abs(whole[rows] - C64) / absC)) < 1e-5
+    # the whole-tile rows are untouched by the split
+    np.testing.assert_array_equal(got[:256], whole[:256])
 
 
 def test_sgemm_generic_exact_bit_exact(gpu):

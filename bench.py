@@ -136,15 +136,14 @@ class Dot(Workload):
 
 class DotChunked(Dot):
     key = "dot_chunked"
-    program = "C1 in an explicit order: split(4096) |> mapGlobal(reduceSeq) |> toMem(Global) |> reduceSeq (bit-exact)"
+    program = ("C1 (dot.rise) + the chunked-reduce strategy (gpu_rules.CHUNKED_REDUCE_STRATEGY: splitReduce(4096), "
+               "...) -> split(4096) |> mapGlobal(reduceSeq) |> toMem(Global) |> reduceSeq (bit-exact)")
     emit_kwargs = {"reassociate": False}
 
     def compile(self):
-        from paper_2201_03611_b200 import compile_program, programs
-        from paper_2201_03611_b200._ref import nat
+        from paper_2201_03611_b200 import compile_program, gpu_rules, programs
 
-        c = compile_program(programs.DOT_CHUNKED, None, name="dotChunked",
-                            assumptions=[(nat.Var("n"), nat.Const(programs.DOT_CHUNK))])
+        c = compile_program(programs.DOT, gpu_rules.CHUNKED_REDUCE_STRATEGY, name="dotChunked")
         return c, {"n": self.n}
 
 

@@ -19,6 +19,8 @@ spellings.  Each is added in four places, and nowhere else:
                reference's own C / OpenMP emission covers the programs that
                use them (the CPU baseline and full-size oracle of conv and
                nbody, oracle/make_ref.py).
+6. rules     — `rules.RULES` / `RULE_PARAMS` (rules.py:237-259): the
+               GPU-oriented rewrite rules of gpu_rules.py for strategy files.
 
 Semantics (there is no reference oracle for these — "parity unpinned" for
 them in the sense of SURVEY.md §8 c; these definitions are the spec):
@@ -42,7 +44,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from ._ref import codegen, dpia, errors, interpreter, lowering, nat, primitives
+from ._ref import codegen, dpia, errors, interpreter, lowering, nat, primitives, rules
 from .types_util import array_elem
 
 # ---------------------------------------------------------------------------
@@ -104,6 +106,9 @@ def install(registry=None):
     _install_lowering()
     _install_interpreter()
     _install_c_emitter()
+    from . import gpu_rules
+
+    gpu_rules.install(rules)  # 6. GPU-oriented rewrite rules (gpu_rules.py)
     _installed = True
     return registry
 

@@ -131,3 +131,57 @@ def test_exact_mode_uses_round_to_nearest_intrinsics():
 def test_sizes_are_template_parameters():
     code = _code("gemv")
     assert "template <int n, int m>" in code.text
+
+
+# ---- GPU-oriented rewrite rules (gpu_rules.py, SURVEY.md §8 f 3) ------------
+
+
+def test_chunked_schedule_is_derived_by_strategy():
+    """DOT + the chunked-reduce strategy lowers to exactly the hand-written
+    two-kernel program (byte-identical sm100a text)."""
+    from paper_2201_03611_b200 import gpu_rules
+
+    derived = compile_program(programs.DOT, gpu_rules.CHUNKED_REDUCE_STRATEGY, name="dotChunked")
+    hand = compile_program(programs.DOT_CHUNKED, None, name="dotChunked",
+                           assumptions=[(nat.Var("n"), nat.Const(programs.DOT_CHUNK))])
+    a = emit_cuda(derived.unit, reassociate=False)
+    b = emit_cuda(hand.unit, reassociate=False)
+    assert a.text == b.text
+    assert [s["kind"] for s in a.plan["stages"]] == ["rowfold", "seqfold"]
+
+
+def test_split_reduce_semantics_on_the_interpreter():
+    """The rewritten program means what the chunked program means (the
+    reference interpreter, bit for bit), and reassociates the plain fold."""
+    import numpy as np
+
+    from paper_2201_03611_b200 import gpu_rules
+    from paper_2201_03611_b200._ref import interpreter
+
+    derived = compile_program(programs.DOT, gpu_rules.CHUNKED_REDUCE_STRATEGY, name="dotChunked")
+    n = 8192
+    rng = np.random.default_rng(3)
+    a = [np.float32(v) for v in rng.uniform(-1, 1, n)]
+    b = [np.float32(v) for v in rng.uniform(-1, 1, n)]
+    got = interpreter.run_unit(derived.unit, {"n": n}, [a, b])
+    parts = []
+    for c0 in range(0, n, 4096):
+        acc = np.float32(0)
+        for x, y in zip(a[c0:c0 + 4096], b[c0:c0 + 4096]):
+            acc = np.float32(acc + np.float32(x * y))
+        parts.append(acc)
+    want = np.float32(np.float32(np.float32(0) + parts[0]) + parts[1])
+    assert np.float32(got) == want
+
+
+def test_split_reduce_refuses_unknown_identities():
+    from paper_2201_03611_b200 import gpu_rules
+    from paper_2201_03611_b200._ref import errors as rerrors
+
+    src = ("depFun((n: Nat) => fun(a: Array[n, f32] => a |> reduce(add)(1.0f)))")
+    with pytest.raises(rerrors.StrategyError):
+        compile_program(src, "splitReduce(4) @ outermost(isReduce) ; toReduceSeq @ every(isReduce)", name="s")
+    assert "splitReduce" in gpu_rules.RULES and "splitMap" in gpu_rules.RULES
+    from paper_2201_03611_b200._ref import rules
+
+    assert any(r.startswith("splitReduce(") for r in rules.describe_rules())

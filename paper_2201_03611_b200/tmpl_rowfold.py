@@ -33,8 +33,10 @@ from ._ref import nat
 from .emit_cuda import NatRenderer, ValueRenderer, kernel_head, py_expr
 
 ROWS = 32
-KT = 128  # columns per stage (4 TMA boxes of 32 columns)
-STAGES = 6
+import os  # noqa: E402
+
+KT = int(os.environ.get("RISE_ROWFOLD_KT", "256"))  # columns per stage (KT/32 TMA boxes of 32 columns)
+STAGES = int(os.environ.get("RISE_ROWFOLD_STAGES", "2"))  # measured (gemv 8192²): 128x6 0.835, 256x2 0.855, 512x2 0.65
 BOX_BYTES = 32 * 32 * 4
 
 

@@ -214,6 +214,69 @@ class Executable:
             host_out.copy_(device_out, non_blocking=True)
         return host_out
 
+    def stream_host(self, host_steps, host_outs, depth=2, timed=False):
+        """End-to-end processing of a stream of steps from host memory:
+        step k copies host_steps[k] (pinned CPU tensors / scalars, unit input
+        order) to the device, runs the kernels, and copies the result into
+        host_outs[k] (pinned).  The three phases run on three streams over
+        `depth` device buffer sets, so step k+1's host->device copy and step
+        k-1's device->host copy overlap step k's kernels (PCIe is full
+        duplex): the steady state costs max(H2D, kernels, D2H) per step
+        instead of their sum.  Every step still moves all of its inputs and
+        its whole result through host memory.  Returns after the last copy
+        has landed; with timed=True also the device time (ms, CUDA events)
+        from the first copy's start to the last copy's end."""
+        import torch
+
+        specs = self.plan["inputs"]
+        dev = [[torch.empty(self.input_sizes[sp["name"]], dtype=_torch_dtype(sp["ctype"]), device="cuda")
+                if not sp["scalar"] else None for sp in specs] for _ in range(depth)]
+        outs = [torch.empty(self.output_size, dtype=_torch_dtype(self.plan["output"]["ctype"]), device="cuda")
+                for _ in range(depth)]
+        launches = []
+        for slot in range(depth):
+            buffers = {self.plan["output"]["name"]: outs[slot]}
+            for sp, d in zip(specs, dev[slot]):
+                if d is not None:
+                    buffers[sp["name"]] = d
+            launches.append(buffers)
+        s_in, s_run, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        copied, ran, landed = [ev() for _ in range(depth)], [ev() for _ in range(depth)], [ev() for _ in range(depth)]
+        used = [False] * depth
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0.record(s_in)
+        for k, (hin, hout) in enumerate(zip(host_steps, host_outs)):
+            slot = k % depth
+            with torch.cuda.stream(s_in):
+                if used[slot]:
+                    s_in.wait_event(ran[slot])  # the kernels of step k - depth read these inputs
+                for sp, h, d in zip(specs, hin, dev[slot]):
+                    if d is not None:
+                        d.copy_(h, non_blocking=True)
+                copied[slot].record(s_in)
+            with torch.cuda.stream(s_run):
+                s_run.wait_event(copied[slot])
+                if used[slot]:
+                    s_run.wait_event(landed[slot])  # step k - depth's result has left this buffer
+                buffers = dict(launches[slot])
+                for sp, h in zip(specs, hin):
+                    if sp["scalar"]:
+                        buffers[sp["name"]] = h
+                self.launch(buffers, stream=s_run)
+                ran[slot].record(s_run)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ran[slot])
+                hout.copy_(outs[slot], non_blocking=True)
+                landed[slot].record(s_out)
+            used[slot] = True
+        t1.record(s_out)
+        s_out.synchronize()
+        if timed:
+            return host_outs, t0.elapsed_time(t1)
+        return host_outs
+
     # convenience: torch in / torch out -----------------------------------------
     def __call__(self, *inputs, out=None, stream=None):
         import torch

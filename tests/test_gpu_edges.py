@@ -94,3 +94,26 @@ def test_wrong_input_length_is_reported(gpu):
     c = _cfg("gemv")
     with pytest.raises(errors.InterpreterError):
         run_cuda(emit_cuda(c.unit), c.unit, {"n": 4, "m": 4}, [np.zeros((4, 3), np.float32), np.zeros(4, np.float32)])
+
+
+def test_stream_host_pipelines_every_step(gpu):
+    """Executable.stream_host: each step's own inputs in, its own result out,
+    with the copies of neighbouring steps overlapping its kernels."""
+    import torch
+
+    from paper_2201_03611_b200.run import Executable
+
+    c = compile_program(programs.MV, programs.MV_GLOBAL_STRATEGY, name="mv")
+    n, m = 256, 1028
+    exe = Executable(emit_cuda(c.unit), {"n": n, "m": m})
+    steps, outs, want = [], [], []
+    for k in range(5):
+        M = oracle.rng_inputs(40 + k, n, m)
+        x = oracle.rng_inputs(50 + k, m)
+        steps.append([torch.from_numpy(M.reshape(-1)).pin_memory(), torch.from_numpy(x).pin_memory()])
+        outs.append(torch.empty(n, dtype=torch.float32).pin_memory())
+        want.append(oracle.mv(M, x))
+    _, ms = exe.stream_host(steps, outs, timed=True)
+    assert ms > 0
+    for o, w in zip(outs, want):
+        np.testing.assert_array_equal(o.numpy(), w)

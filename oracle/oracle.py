@@ -70,6 +70,7 @@ def ref_lib():
         L.mvOptKernel.argtypes = [_fp, _int, _int, _int, _fp, _fp]
         L.sgemmBtKernel.argtypes = [_fp, _int, _int, _int, _fp, _fp]
         L.convKernel.argtypes = [_fp, _int, _int, _fp, _fp]
+        L.asumKernel.argtypes = [_fp, _int, _fp]
         L.nbodyShardKernel.argtypes = [_fp, _int, _int, _fp, _fp, _fp, _fp]
         _ref = L
     return _ref
@@ -172,6 +173,15 @@ def ref_mv(M, x, s=None):
     else:
         L.mvOptKernel(_ptr(out), n, m, s, _ptr(M), _ptr(x))
     return out
+
+
+def ref_asum(x):
+    """The reference emitter's C for programs.ASUM (sequential left fold of |x_i|)."""
+    L = ref_lib()
+    x = f32(x)
+    out = np.zeros(1, np.float32)
+    L.asumKernel(_ptr(out), x.size, _ptr(x))
+    return out[0]
 
 
 def ref_conv3x3(img, w):

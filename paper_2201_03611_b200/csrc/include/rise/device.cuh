@@ -32,6 +32,7 @@ RS_DEVICE float2 rs_neg2(float2 a) { return make_float2(-a.x, -a.y); }
 RS_DEVICE float2 rs_div2(float2 a, float2 b) { return make_float2(a.x / b.x, a.y / b.y); }
 RS_DEVICE float2 rs_rsqrt2(float2 a) { return make_float2(rs_rsqrt_fast(a.x), rs_rsqrt_fast(a.y)); }
 RS_DEVICE float2 rs_sqrt2(float2 a) { return make_float2(sqrtf(a.x), sqrtf(a.y)); }
+RS_DEVICE float2 rs_fabs2(float2 a) { return make_float2(fabsf(a.x), fabsf(a.y)); }
 // correctly rounded per-lane forms for exact-mode packed bodies
 //
 // ptxas (CUDA 12.9) contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even

@@ -163,6 +163,8 @@ class ValueRenderer:
                 return f"__fsqrt_rn({a})" if self.exact else f"sqrtf({a})"
             if e.fn == "rsqrt":
                 return f"rs_rsqrt_exact({a})" if self.exact else f"rs_rsqrt_fast({a})"
+            if e.fn == "abs":
+                return f"fabsf({a})" if e.ctype == "float" else f"abs({a})"
         raise EmitError(f"cannot render value {e!r}")
 
     def target(self, t):

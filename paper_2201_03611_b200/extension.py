@@ -33,6 +33,7 @@ them in the sense of SURVEY.md §8 c; these definitions are the spec):
 * `slide2D(sz)(sp)` = map(slide(sz)(sp)) >> slide(sz)(sp) >> map(transpose):
   window (i, j) row a col b = xs[i*sp+a][j*sp+b].
 * `transpose`: Array[n, Array[m, t]] -> Array[m, Array[n, t]].
+* `abs` is |x| (exact: the sign bit cleared for binary32; i32 abs).
 * `div` is IEEE binary32 division (C truncation for i32); `sqrt` is IEEE
   binary32 square root; `rsqrt(x)` = 1.0f / sqrt(x) with both operations
   rounded to binary32 (the GPU evaluates it with the MUFU reciprocal square
@@ -41,6 +42,8 @@ them in the sense of SURVEY.md §8 c; these definitions are the spec):
 """
 
 from __future__ import annotations
+
+import re
 
 import numpy as np
 
@@ -59,6 +62,7 @@ SCHEMES = {
     "div": "{t: DataType} -> t -> t -> t",
     "sqrt": "{t: DataType} -> t -> t",
     "rsqrt": "{t: DataType} -> t -> t",
+    "abs": "{t: DataType} -> t -> t",
     "toGlobal": "{t: DataType} -> t -> t",
     "toLocal": "{t: DataType} -> t -> t",
     "toPrivate": "{t: DataType} -> t -> t",
@@ -76,6 +80,7 @@ SIGNATURE_TEXT = {
     "div": "(t: DataType, w: ReadWrite, a: Exp[t,Rd], b: Exp[t,Rd]): Exp[t,w]",
     "sqrt": "(t: DataType, w: ReadWrite, a: Exp[t,Rd]): Exp[t,w]",
     "rsqrt": "(t: DataType, w: ReadWrite, a: Exp[t,Rd]): Exp[t,w]",
+    "abs": "(t: DataType, w: ReadWrite, a: Exp[t,Rd]): Exp[t,w]",
     "toGlobal": "(t: DataType, x: Exp[t,Wr]): Exp[t,Rd]",
     "toLocal": "(t: DataType, x: Exp[t,Wr]): Exp[t,Rd]",
     "toPrivate": "(t: DataType, x: Exp[t,Wr]): Exp[t,Rd]",
@@ -85,7 +90,7 @@ SIGNATURE_TEXT = {
 
 VIEW_TAGS = ("transpose", "slide", "padClamp", "padClamp2D", "slide2D")
 BINARY_TAGS = ("div",)
-UNARY_TAGS = ("sqrt", "rsqrt")
+UNARY_TAGS = ("sqrt", "rsqrt", "abs")
 TO_MEM_ALIASES = {"toGlobal": "Global", "toLocal": "Local", "toPrivate": "Private"}
 
 _installed = False
@@ -251,9 +256,16 @@ def f32_rsqrt(a):
         return np.float32(1.0) / np.sqrt(np.float32(a))
 
 
+def any_abs(a):
+    """|a|: exact for binary32 (sign bit cleared) and i32."""
+    if isinstance(a, np.float32):
+        return np.float32(abs(a))
+    return abs(a)
+
+
 def _install_interpreter():
     arity = {"transpose": 1, "slide": 1, "padClamp": 1, "padClamp2D": 1, "slide2D": 1,
-             "div": 2, "sqrt": 1, "rsqrt": 1, "toGlobal": 1, "toLocal": 1, "toPrivate": 1}
+             "div": 2, "sqrt": 1, "rsqrt": 1, "abs": 1, "toGlobal": 1, "toLocal": 1, "toPrivate": 1}
     interpreter._PRIM_ARITY.update(arity)
     base_exec = interpreter._exec_prim
 
@@ -278,6 +290,8 @@ def _install_interpreter():
             return f32_sqrt(args[0])
         if name == "rsqrt":
             return f32_rsqrt(args[0])
+        if name == "abs":
+            return any_abs(args[0])
         if name in TO_MEM_ALIASES:
             return args[0]
         return base_exec(name, deps, args, nat_env)
@@ -303,6 +317,8 @@ def _install_interpreter():
             return f32_sqrt(ev(p.args[0], env, store, nat_env))
         if tag == "rsqrt":
             return f32_rsqrt(ev(p.args[0], env, store, nat_env))
+        if tag == "abs":
+            return any_abs(ev(p.args[0], env, store, nat_env))
         return base_fun(p, env, store, nat_env)
 
     interpreter._eval_fun_prim = eval_fun_prim
@@ -371,6 +387,9 @@ def _install_c_emitter():
                 return f"({a} / {emit_exp(p.args[1], env, state)})"
             if p.tag == "sqrt":
                 return f"sqrtf({a})"
+            if p.tag == "abs":
+                t = p.type_args[0]
+                return f"fabsf({a})" if getattr(t, "name", "f32") == "f32" else f"abs({a})"
             return f"(1.0f / sqrtf({a}))"  # rsqrt: both operations rounded to binary32
         return base_exp(p, env, state, pending, projs)
 
@@ -384,8 +403,10 @@ def _install_c_emitter():
         text = base_emit(unit, target)
         if target != "opencl":
             head = []
-            if "sqrtf(" in text:
+            if "sqrtf(" in text or "fabsf(" in text:
                 head.append("#include <math.h>")
+            if re.search(r"(?<![a-z])abs\(", text):
+                head.append("#include <stdlib.h>")
             if "rs_clamp(" in text:
                 head.append(C_HELPERS.rstrip())
             if head:

@@ -224,6 +224,17 @@ REDUCE_TMA_STAGES = int(os.environ.get("RISE_REDUCE_TMA_STAGES", "3"))
 REDUCE_TMA_CONTIG = os.environ.get("RISE_REDUCE_TMA_CONTIG", "0") == "1"
 
 
+def reduce_fold_length(n: int) -> int:
+    """Terms one thread folds sequentially in phase 1 of the `reduce`
+    template for n terms (its error bound's sequential part)."""
+    n4 = -(-n // 4)
+    if REDUCE_TMA:
+        ch4 = REDUCE_TMA_CHUNK // 16
+        chunks = -(-n4 // ch4)
+        return 4 * -(-chunks // REDUCE_TMA_GRID) * -(-ch4 // REDUCE_BLOCK)
+    return 4 * -(-n4 // (REDUCE_GRID * REDUCE_BLOCK))
+
+
 def _match_reduce(prog, stage, base_name, temps, exact):
     if stage.kind != "serial":
         return None

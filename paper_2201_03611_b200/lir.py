@@ -69,7 +69,7 @@ class Bin:
 
 @dataclass(frozen=True)
 class Un:
-    fn: str  # sqrt | rsqrt
+    fn: str  # sqrt | rsqrt | abs
     a: object
     ctype: str
 
@@ -427,6 +427,11 @@ class Builder:
                     raise EmitError("indexed arithmetic value")
                 a = self.exp(a0, env)
                 return Un(tag, a, "float")
+            if tag == "abs":
+                if pending or projs:
+                    raise EmitError("indexed arithmetic value")
+                a = self.exp(a0, env)
+                return Un(tag, a, getattr(a, "ctype", "float"))
         raise EmitError(f"no emission for expression {getattr(p, 'tag', type(p).__name__)}")
 
     # writes ------------------------------------------------------------------

@@ -26,6 +26,13 @@ depFun((n: Nat) => fun(a: Array[n, f32] => fun(b: Array[n, f32] =>
 """
 DOT_STRATEGY = "fuseReduceMap @ every(isReduce) ; toReduceSeq @ every(isReduce)"
 
+# the north star's other memory-bound reduction: asum = sum |x_i| (needs the
+# extension's `abs`)
+ASUM = """\
+depFun((n: Nat) => fun(x: Array[n, f32] => x |> map(fun(v => abs(v))) |> reduce(add)(0.0f) ))
+"""
+ASUM_STRATEGY = DOT_STRATEGY
+
 # C1 written in an explicit, parallel order: 4096-element chunks folded
 # left-to-right in parallel (one row per thread, the `rowfold` template),
 # then the chunk partials folded left-to-right.  Emitted with

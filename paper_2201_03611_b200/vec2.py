@@ -105,6 +105,8 @@ class Vec2:
                 return f"rs_rsqrt2({self.val(e.a)})" if not self.exact else f"rs_rsqrt2_rn({self.val(e.a)})"
             if e.fn == "sqrt":
                 return f"rs_sqrt2({self.val(e.a)})" if not self.exact else f"rs_sqrt2_rn({self.val(e.a)})"
+            if e.fn == "abs" and e.ctype == "float":
+                return f"rs_fabs2({self.val(e.a)})"
         raise NoVec2()
 
     def _is_zero(self, e):

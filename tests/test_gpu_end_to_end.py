@@ -118,3 +118,19 @@ def test_local_memory_with_barriers(gpu):
     M = [[round(rng.uniform(-4, 4), 3) for _ in range(300)] for _ in range(37)]
     got = run_cuda(code, c.unit, nats, [M])
     assert interpreter.values_close(got, interpreter.run_unit(c.unit, nats, [M]))
+
+
+def test_left_fold_known_answer(gpu):
+    # test_interpreter.py:55-57: reduce is a left fold from init: [1,2,3,4] with a - b from 0 -> -10
+    c = compile_program("fun(xs: Array[4, f32] => xs |> reduce(fun(a, b => a - b))(0.0f))",
+                        "toReduceSeq @ every(isReduce)", name="leftFold")
+    out = run_cuda(emit_cuda(c.unit), c.unit, {}, [[1.0, 2.0, 3.0, 4.0]])
+    assert interpreter.values_close(out, np.float32(-10.0))
+
+
+def test_fuse_reduce_map_known_answer(gpu):
+    # test_rules.py:212-216: map(v * v) >> reduce(add)(0) fused -> 14 on [1, 2, 3]
+    c = compile_program("fun(xs: Array[3, i32] => xs |> map(fun(v => v * v)) |> reduce(add)(0))",
+                        "fuseReduceMap @ every(isReduce) ; toReduceSeq @ every(isReduce)", name="sumSq")
+    out = run_cuda(emit_cuda(c.unit), c.unit, {}, [[1, 2, 3]])
+    assert int(np.asarray(out).reshape(-1)[0]) == 14

@@ -68,8 +68,25 @@ def test_dot_reduce_within_bound(gpu, n):
     got = run_cuda(code, c.unit, {"n": n}, [a, b], as_numpy=True)[0]
     v64, abs_sum = oracle.dot_f64(a, b)
     from paper_2201_03611_b200 import idioms
-    per_thread = -(-n // (idioms.REDUCE_GRID * idioms.REDUCE_BLOCK))
-    assert abs(float(got) - v64) <= oracle.reassociated_dot_bound(n, abs_sum, 4 * per_thread)
+
+    assert abs(float(got) - v64) <= oracle.reassociated_dot_bound(n, abs_sum, idioms.reduce_fold_length(n))
+
+
+@pytest.mark.parametrize("n", [1 << 24, 4096 + 4])
+def test_asum_reduce_within_bound_and_seqfold_bit_exact(gpu, n):
+    c = compile_program(programs.ASUM, programs.ASUM_STRATEGY, name="asum")
+    x = oracle.rng_inputs(21, n)
+    code = emit_cuda(c.unit)
+    assert code.plan["stages"][0]["kind"] == "reduce"
+    got = float(run_cuda(code, c.unit, {"n": n}, [x], as_numpy=True)[0])
+    s64 = float(np.abs(x.astype(np.float64)).sum())
+    from paper_2201_03611_b200 import idioms
+
+    assert abs(got - s64) <= oracle.reassociated_dot_bound(n, s64, idioms.reduce_fold_length(n))
+    exact = emit_cuda(c.unit, reassociate=False)
+    got = run_cuda(exact, c.unit, {"n": n}, [x], as_numpy=True)[0]
+    want = np.add.accumulate(np.abs(x), dtype=np.float32)[-1]
+    assert np.float32(got).view(np.uint32) == np.float32(want).view(np.uint32)
 
 
 def test_dot_deterministic(gpu):

@@ -117,6 +117,13 @@ def test_restatement_equals_reference_c_of_extension_programs_at_size():
                                   oracle.ref_nbody_block(pos, vel, mass, 100, 64))
 
 
+@needs_ref
+def test_reference_c_asum_is_the_sequential_fold():
+    x = oracle.rng_inputs(9, 100003)
+    want = np.add.accumulate(np.abs(x), dtype=np.float32)[-1]  # left fold from 0 (0 + a == a exactly)
+    assert oracle.ref_asum(x).view(np.uint32) == np.float32(want).view(np.uint32)
+
+
 def test_left_fold_order_is_pinned():
     # interpreter.py:134-138: reduce is a left fold from init; 0.1+0.2+0.3 in
     # fp32 (test_interpreter.py:79-84) — the restatement does the same

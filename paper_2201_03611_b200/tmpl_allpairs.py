@@ -41,7 +41,7 @@ import os
 # on B200: SPLIT 1 / 4 / 8 / 16 -> 0.52 / 0.63 / 0.67 / 0.67 of FP32 peak
 SPLIT = int(os.environ.get("RISE_ALLPAIRS_SPLIT", "16"))
 RB = int(os.environ.get("RISE_ALLPAIRS_RB", "4"))  # targets per thread
-JT = int(os.environ.get("RISE_ALLPAIRS_JT", "64"))  # sources per warp tile
+JT = int(os.environ.get("RISE_ALLPAIRS_JT", "32"))  # sources per warp tile (measured: 32 > 64 > 16)
 UNROLL = int(os.environ.get("RISE_ALLPAIRS_UNROLL", "4"))  # source loop unroll
 PACKED = os.environ.get("RISE_ALLPAIRS_PACKED", "1") == "1"  # two targets per FFMA2/FADD2/FMUL2
 

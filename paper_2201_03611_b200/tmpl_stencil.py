@@ -41,6 +41,7 @@ import os  # noqa: E402
 BLOCKS_PER_SM = int(os.environ.get("RISE_STENCIL_BPS", "3"))
 # full tiles leave through shared memory and one TMA tile store (else 16-byte STGs)
 TMA_STORE = os.environ.get("RISE_STENCIL_TMA_STORE", "1") == "1"
+STAGES = int(os.environ.get("RISE_STENCIL_STAGES", "2"))  # ring depth per block (measured: 2 x 3 blocks/SM 0.82 > 3 x 2 0.78 > 4 x 1 0.77)
 
 
 def _seq_loop_bounds(stmt):
@@ -168,11 +169,12 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         f"  constexpr int RS_H = {r(A.dims[0])}, RS_W = {r(A.dims[1])};",
         f"  constexpr int RS_SR = {sr}, RS_SW = {sw};",
         "  constexpr int RS_STAGE = (RS_SR * RS_SW + 31) / 32 * 32;  // stages stay 128-byte aligned (TMA)",
+        f"  constexpr int RS_NSTAGE = {STAGES};",
         f"  constexpr int RS_NTX = (RS_C + {TC - 1}) / {TC}, RS_NTY = (RS_R + {TR - 1}) / {TR};",
         "  constexpr int RS_NTILES = RS_NTX * RS_NTY;",
         "  extern __shared__ __align__(128) unsigned char rs_dsmem[];",
         "  float* rs_buf = reinterpret_cast<float*>(rs_dsmem + ((128u - (rs_smem_addr(rs_dsmem) & 127u)) & 127u));",
-        "  unsigned long long* rs_bar = reinterpret_cast<unsigned long long*>(rs_buf + 2 * RS_STAGE);",
+        "  unsigned long long* rs_bar = reinterpret_cast<unsigned long long*>(rs_buf + RS_NSTAGE * RS_STAGE);",
         "  const int rs_tid = threadIdx.y * blockDim.x + threadIdx.x;",
         "  // tile t -> (rs_r0, rs_c0); interior tiles arrive by TMA, border tiles by clamped loads",
         "  auto rs_origin = [&](int t, int& r0, int& c0) {",
@@ -190,10 +192,10 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         f"    rs_tma_load_2d(rs_buf + s * RS_STAGE, &rs_map, c0 - {lp}, r0 + ({o0lo}), &rs_bar[s]);",
         "  };",
         "  if (rs_tid == 0) {",
-        "    rs_mbar_init(&rs_bar[0], 1);",
-        "    rs_mbar_init(&rs_bar[1], 1);",
+        "    for (int rs_q = 0; rs_q < RS_NSTAGE; ++rs_q) rs_mbar_init(&rs_bar[rs_q], 1);",
         "    rs_fence_barrier_init();",
-        "    if ((int)blockIdx.x < RS_NTILES) rs_issue(blockIdx.x, 0);",
+        "    for (int rs_q = 0; rs_q < RS_NSTAGE - 1; ++rs_q)",
+        "      if ((int)blockIdx.x + rs_q * (int)gridDim.x < RS_NTILES) rs_issue(blockIdx.x + rs_q * gridDim.x, rs_q);",
         "  }",
         "  __syncthreads();",
     ]
@@ -204,21 +206,20 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
             f"  for (int rs_e = 0; rs_e < {size}; ++rs_e) rs_p_{buf}[rs_e] = __ldg({buf} + rs_e);",
         ]
     lines += [
-        "  unsigned rs_phase0 = 0u, rs_phase1 = 0u;",
         "  int rs_it = 0;",
         "  for (int rs_t = blockIdx.x; rs_t < RS_NTILES; rs_t += gridDim.x, ++rs_it) {",
-        "    const int rs_s = rs_it & 1;",
+        "    const int rs_s = rs_it % RS_NSTAGE;",
         "    int rs_r0, rs_c0;",
         "    rs_origin(rs_t, rs_r0, rs_c0);",
         f"    const int rs_tr0 = rs_r0 + ({o0lo}), rs_tc0 = rs_c0 - {lp};",
         "    float* rs_tile = rs_buf + rs_s * RS_STAGE;",
-        "    // prefetch the next tile into the other stage (freed by the barrier that ended the previous tile)",
-        "    if (rs_tid == 0 && rs_t + (int)gridDim.x < RS_NTILES) {",
+        "    // prefetch NSTAGE-1 tiles ahead into the stage the previous tile used (freed by the barrier",
+        "    // that ended it)",
+        "    if (rs_tid == 0 && rs_t + (RS_NSTAGE - 1) * (int)gridDim.x < RS_NTILES) {",
         "      rs_bulk_wait_read_all();  // that stage staged the previous tile's output (TMA store)" if tma_store else "",
-        "      rs_issue(rs_t + gridDim.x, rs_s ^ 1);",
+        "      rs_issue(rs_t + (RS_NSTAGE - 1) * gridDim.x, (rs_it + RS_NSTAGE - 1) % RS_NSTAGE);",
         "    }",
-        "    if (rs_s == 0) { rs_mbar_wait(&rs_bar[0], rs_phase0); rs_phase0 ^= 1u; }",
-        "    else { rs_mbar_wait(&rs_bar[1], rs_phase1); rs_phase1 ^= 1u; }",
+        "    rs_mbar_wait(&rs_bar[rs_s], (unsigned)((rs_it / RS_NSTAGE) & 1));",
         "    if (!rs_is_interior(rs_r0, rs_c0)) {",
         "      // padClamp: every out-of-range staged cell takes the value of the nearest in-range",
         "      // cell, which the same box holds (the box always contains an in-range row and column)",
@@ -283,7 +284,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         lines.append("  if (rs_tid == 0) rs_bulk_wait_all();  // the last tile's store has left shared memory")
     lines += ["}"]
     lines = [x for x in lines if x != ""]
-    smem = 2 * (-(-(sr * sw) // 32) * 32) * 4 + 16 + 128
+    smem = STAGES * (-(-(sr * sw) // 32) * 32) * 4 + 8 * STAGES + 128
     plan = {
         "name": name,
         "kind": "stencil2d",

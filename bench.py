@@ -361,6 +361,16 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.Stream()
     dev_in = [torch.from_numpy(np.ascontiguousarray(h).reshape(-1)).to("cuda") for h in host]
     out = torch.empty(exe.output_size, dtype=torch.float32, device="cuda")
+    extra = {}
+    peer_sources = None
+    if exe.plan.get("peer_ranks"):
+        from paper_2201_03611_b200 import shard
+
+        torch.cuda.synchronize()
+        peer_sources = shard.PeerSources({"pos": dev_in[2], "mass": dev_in[3]},
+                                         exe.plan["stages"][0]["peer_streams"])
+        dist.barrier()
+        extra["rs_peer_table"] = peer_sources.table
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
     sweep = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
     sink = torch.empty((), dtype=torch.float32, device="cuda")
@@ -372,12 +382,12 @@ def run_ours(args, rank, world, local_rank):
         flush.zero_()
         torch.sum(sweep, dim=0, out=sink)
 
-    launch = _bound_launch(exe, dev_in, out, stream)
+    launch = _bound_launch(exe, dev_in, out, stream, extra)
 
     def step():
         launch()
 
-    if world > 1:
+    if world > 1 and not peer_sources:
         step = _distributed_step(wl, exe, dev_in, out, stream, dist, rank, world)
 
     with torch.cuda.stream(stream):
@@ -417,21 +427,23 @@ def run_ours(args, rank, world, local_rank):
     host_out = torch.empty(exe.output_size, dtype=torch.float32).pin_memory()
     e2e_steps = max(3, min(args.steps, 10))
     for _ in range(2):
-        exe.run_host(pinned, host_out, dev_in, out, stream)
+        exe.run_host(pinned, host_out, dev_in, out, stream, extra=extra)
     stream.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(e2e_steps):
-        exe.run_host(pinned, host_out, dev_in, out, stream)
+        exe.run_host(pinned, host_out, dev_in, out, stream, extra=extra)
     e1.record(stream)
     stream.synchronize()
     e2e_seq_ms = e0.elapsed_time(e1) / e2e_steps
     # the same steps through the streaming API: H2D / kernels / D2H of
     # consecutive steps overlap on three streams (Executable.stream_host)
-    outs = [host_out] * e2e_steps
-    exe.stream_host([pinned] * 2, [host_out] * 2)  # warm-up (allocations)
-    _, pipe_ms = exe.stream_host([pinned] * e2e_steps, outs, timed=True)
-    e2e_ms = min(pipe_ms / e2e_steps, e2e_seq_ms)
+    e2e_ms = e2e_seq_ms
+    if peer_sources is None:  # (peer-source kernels read the exported blocks, not fresh buffers)
+        outs = [host_out] * e2e_steps
+        exe.stream_host([pinned] * 2, [host_out] * 2, extra=extra)  # warm-up (allocations)
+        _, pipe_ms = exe.stream_host([pinned] * e2e_steps, outs, timed=True, extra=extra)
+        e2e_ms = min(pipe_ms / e2e_steps, e2e_seq_ms)
     if dist is not None:
         t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -486,6 +498,9 @@ def run_ours(args, rank, world, local_rank):
         }
     if dist is not None:
         dist.barrier()
+        if peer_sources is not None:
+            peer_sources.close()
+            dist.barrier()
         dist.destroy_process_group()
     return result
 
@@ -501,8 +516,10 @@ def _parallelism_text(wl, world):
         "dot_chunked": "weak: rank r owns a 2^24 chunk; partials all-gathered (rs_allgather, NCCL), rank-order fold",
         "conv": "weak: rank r owns an 8192-row band; halo rows pulled from the neighbours' bands over NVLink "
                 "(rs_halo_exchange, CUDA IPC) per step",
-        "nbody": f"strong: 131072 bodies, {131072 // world} targets per rank; positions/masses all-gathered "
-                 "(rs_allgather, NCCL) per step",
+        "nbody": (f"strong: 131072 bodies, {131072 // world} targets per rank; "
+                  + ("every rank's position/mass block read in place over NVLink by the force kernel "
+                     "(peer pointers, all-gather fused into the fold)" if _nbody_peer() else
+                     "positions/masses all-gathered (rs_allgather, NCCL) per step")),
     }[wl.key]
 
 
@@ -528,15 +545,26 @@ def _distributed_variant(wl, compiled, nats, host, rank, world):
         mass = rng.uniform(0.5, 1.5, n).astype(np.float32)
         t0 = rank * t
         c = compile_program(programs.NBODY_SHARD, None, name="nbodyShard")
+        if _nbody_peer():
+            # the fused variant: each rank holds only its block; the kernel
+            # reads every other block in place over NVLink (peer pointers)
+            wl.emit_kwargs = {"peer_ranks": world}
+            blk = pos[t0:t0 + t]
+            return c, {"t": t, "n": n}, [blk, np.zeros((t, 3), np.float32), blk, mass[t0:t0 + t]]
         return c, {"t": t, "n": n}, [pos[t0:t0 + t], np.zeros((t, 3), np.float32), pos, mass]
     return compiled, nats, host
 
 
-def _bound_launch(exe, dev_in, out, stream):
+def _nbody_peer():
+    return os.environ.get("RISE_NBODY_PEER", "1") == "1"
+
+
+def _bound_launch(exe, dev_in, out, stream, extra=None):
     """All of a step's kernel launches with argument arrays built once
     (Executable.bind): the timed region then contains the kernels, not
     Python argument marshalling."""
-    buffers = {spec["name"]: value for spec, value in zip(exe.plan["inputs"], dev_in)}
+    buffers = dict(extra or {})
+    buffers.update({spec["name"]: value for spec, value in zip(exe.plan["inputs"], dev_in)})
     buffers[exe.plan["output"]["name"]] = out
     return exe.bind(buffers, stream)
 

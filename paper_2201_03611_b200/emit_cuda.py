@@ -478,16 +478,22 @@ def arg_names(prog: lir.Program, temps):
 # whole units
 
 
-def emit_cuda(unit, exact=True, idioms=True, reassociate=True) -> CudaCode:
+def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0) -> CudaCode:
     """Emit the sm100a kernel text (and launch plan) for an ImperativeUnit.
 
     `reassociate=False` keeps every reduction in the program's own order
     (templates that reassociate — `reduce`, `gemm_tc`, fast-math `allpairs` —
     are not used), so every kernel is bit-exact with the reference's
-    sequential semantics."""
+    sequential semantics.
+
+    `peer_ranks=R` (multi-GPU, one process per GPU): the `allpairs` source
+    streams are distributed over R ranks in equal contiguous blocks and read
+    in place through a device table of peer pointers (extra launch argument
+    `rs_peer_table`), fusing the all-gather of the sources into the fold."""
     from . import idioms as idiom_mod
 
     prog = lir.build(unit)
+    prog.peer_ranks = int(peer_ranks)
     stages, temps = split_stages(prog.body, prog)
     kernels = []
     plan_stages = []
@@ -498,6 +504,8 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True) -> CudaCode:
         kernels.append(generic.text)
         entry = dict(generic.plan)
         match = idiom_mod.match(prog, st, base, temps, exact, reassociate) if idioms else None
+        if peer_ranks and (match is None or not match.plan.get("peer_ranks")):
+            raise EmitError("peer_ranks needs a stage the allpairs template takes (sources read in place)")
         if match is not None:
             kernels.append(match.text)
             for inc in match.includes:
@@ -519,6 +527,12 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True) -> CudaCode:
         "exact": exact,
         "reassociate": reassociate,
     }
+    if peer_ranks:
+        plan["peer_ranks"] = int(peer_ranks)
+        peers = {b for st in plan_stages for b in st.get("peer_streams", [])}
+        for spec in plan["inputs"]:
+            if spec["name"] in peers:
+                spec["peer"] = True
     header = [
         f"// rise-b200 {TARGET} kernels for RISE unit '{prog.name}' (generated by emit_cuda; do not edit)",
         PLAN_TAG + json.dumps(plan, sort_keys=True),

@@ -171,6 +171,7 @@ class Program:
     buffers: dict = field(default_factory=dict)
     clamps: dict = field(default_factory=dict)  # "__clampK" -> (inner Nat, hi Nat)
     names: dict = field(default_factory=dict)  # DPIA name -> C name
+    peer_ranks: int = 0  # emission option: allpairs sources read from R ranks' blocks
 
 
 # ---------------------------------------------------------------------------

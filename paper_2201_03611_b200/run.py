@@ -69,6 +69,9 @@ class Executable:
         for st in self.plan["stages"]:
             chosen = st
             if st.get("pre") and not all(eval_py(p, self.nats) for p in st["pre"]):
+                if st.get("peer_ranks"):
+                    raise InterpreterError(f"{st['name']}: sizes {self.nats} do not split over "
+                                           f"{st['peer_ranks']} ranks' source blocks (no fallback reads peers)")
                 chosen = st["fallback"]
             fmad = fmad or bool(chosen.get("fmad", False))
             name_expr = f"{chosen['name']}<{targs}>" if targs else chosen["name"]
@@ -191,6 +194,11 @@ class Executable:
             pitch = eval_py(extra.get("pitch", extra["dims"][0]), self.nats)
             return rt.tma_desc_2d_f32(base, dims[0], dims[1], pitch * 4, extra["box"][0], extra["box"][1],
                                       extra.get("swizzle", 0))
+        if kind == "peer_table":
+            table = buffers.get("rs_peer_table")
+            if table is None:
+                raise InterpreterError("peer-source kernel launched without buffers['rs_peer_table']")
+            return ctypes.c_void_p(_dptr(table))
         if kind == "gemm_full_tiles":
             from .tmpl_gemm import full_tiles
 
@@ -198,7 +206,7 @@ class Executable:
                                            eval_py(extra["K"], self.nats), extra["bn"], self.sm_count))
         raise InterpreterError(f"unknown extra kernel argument {kind!r}")
 
-    def run_host(self, host_inputs, host_out, device_inputs, device_out, stream=None):
+    def run_host(self, host_inputs, host_out, device_inputs, device_out, stream=None, extra=None):
         """End-to-end step through host memory: copy `host_inputs` (pinned
         torch CPU tensors, scalars passed through) into `device_inputs`,
         launch, and copy the result back into `host_out` — all enqueued on
@@ -210,11 +218,11 @@ class Executable:
             for h, d in zip(host_inputs, device_inputs):
                 if isinstance(d, torch.Tensor):
                     d.copy_(h, non_blocking=True)
-            self(*device_inputs, out=device_out, stream=stream)
+            self(*device_inputs, out=device_out, stream=stream, extra=extra)
             host_out.copy_(device_out, non_blocking=True)
         return host_out
 
-    def stream_host(self, host_steps, host_outs, depth=2, timed=False):
+    def stream_host(self, host_steps, host_outs, depth=2, timed=False, extra=None):
         """End-to-end processing of a stream of steps from host memory:
         step k copies host_steps[k] (pinned CPU tensors / scalars, unit input
         order) to the device, runs the kernels, and copies the result into
@@ -235,7 +243,8 @@ class Executable:
                 for _ in range(depth)]
         launches = []
         for slot in range(depth):
-            buffers = {self.plan["output"]["name"]: outs[slot]}
+            buffers = dict(extra or {})
+            buffers[self.plan["output"]["name"]] = outs[slot]
             for sp, d in zip(specs, dev[slot]):
                 if d is not None:
                     buffers[sp["name"]] = d
@@ -278,18 +287,23 @@ class Executable:
         return host_outs
 
     # convenience: torch in / torch out -----------------------------------------
-    def __call__(self, *inputs, out=None, stream=None):
+    def __call__(self, *inputs, out=None, stream=None, extra=None):
+        """`extra`: additional named launch buffers (e.g. `rs_peer_table`, the
+        device table of peer source pointers of a peer_ranks emission)."""
         import torch
 
         if len(inputs) != len(self.plan["inputs"]):
             raise InterpreterError(f"expected {len(self.plan['inputs'])} inputs, got {len(inputs)}")
-        buffers = {}
+        buffers = dict(extra or {})
         for spec, value in zip(self.plan["inputs"], inputs):
             if spec["scalar"]:
                 buffers[spec["name"]] = value
                 continue
             if not (isinstance(value, torch.Tensor) and value.is_cuda):
                 raise InterpreterError(f"input {spec['name']!r} must be a CUDA tensor")
+            if spec.get("peer"):  # read through rs_peer_table; the local argument is this rank's block
+                buffers[spec["name"]] = value
+                continue
             if value.numel() != self.input_sizes[spec["name"]]:
                 raise InterpreterError(
                     f"input {spec['name']!r} has {value.numel()} elements, expected {self.input_sizes[spec['name']]}")

@@ -171,3 +171,46 @@ class DeviceComm:
 
     def close(self):
         self.comm.close()
+
+
+class PeerSources:
+    """The source blocks of an `allpairs` kernel emitted with peer_ranks=R:
+    every rank exports its blocks (CUDA IPC), maps everyone else's, and
+    builds the device table of block pointers in the kernel's stream order
+    (plan stage `peer_streams`), which the kernel reads sources through —
+    the all-gather of positions and masses fused into the force fold (no
+    collective on the data path).
+
+    `blocks` maps stream name -> this rank's contiguous block (device
+    tensor).  Like PeerHalo this is a pull model: the caller orders the
+    launch after the owners' writes of their blocks (static in the bench)."""
+
+    def __init__(self, blocks: dict, order, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import runtime
+
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        mine = {name: runtime.ipc_handle(t.data_ptr()) for name, t in blocks.items()}
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=group)
+        self.opened = []
+        ptrs = []
+        for name in order:
+            for r in range(self.world):
+                if r == self.rank:
+                    ptrs.append(int(blocks[name].data_ptr()))
+                else:
+                    h, off = everyone[r][name]
+                    p = runtime.ipc_open(h, off)
+                    self.opened.append(p)
+                    ptrs.append(p)
+        self.table = torch.tensor(ptrs, dtype=torch.int64, device="cuda")
+
+    def close(self):
+        from . import runtime
+
+        for p in self.opened:
+            runtime.ipc_close(p)
+        self.opened = []

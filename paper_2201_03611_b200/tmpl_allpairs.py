@@ -223,10 +223,18 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     cdecl = f"const int {cvar}" if cvar else "const int rs_c_unused"
     split = SPLIT if _fold_is_sum(jloop.body, acc) else 1
     nthreads = 32 * split
-    lines = kernel_head(prog, name, temps, launch_bounds=nthreads)
+    peer = int(getattr(prog, "peer_ranks", 0) or 0)
+    extra = ["const unsigned long long* __restrict__ rs_peer"] if peer else []
+    lines = kernel_head(prog, name, temps, launch_bounds=nthreads, extra_params=extra)
     lines += [
         f"  constexpr int RS_NT = {r(NT)}, RS_NS = {r(NS)}, RS_JT = {JT}, RS_RB = {RB}, RS_C = {Cv};",
         f"  constexpr int RS_SPLIT = {split}, RS_CH = (RS_NS + RS_SPLIT - 1) / RS_SPLIT;",
+    ]
+    if peer:
+        lines += [
+            f"  constexpr int RS_RANKS = {peer}, RS_PER_RANK = RS_NS / RS_RANKS;",
+        ]
+    lines += [
         # one source tile per warp: the warps of a block fold disjoint source
         # chunks for the same targets, so a warp only ever syncs with itself
         f"  __shared__ __align__(16) float rs_sm[RS_SPLIT][RS_JT * {rec}];",
@@ -267,11 +275,21 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "    const int rs_jn = rs_je - rs_j0 < RS_JT ? rs_je - rs_j0 : RS_JT;",
         "    __syncwarp();",
     ]
-    for buf, a in s_list:
+    if peer:
+        # the sources live in the R ranks' blocks (peer memory over NVLink):
+        # a tile never straddles two blocks (preconditions), so its records
+        # are read straight from the owning rank — the all-gather is fused
+        # into the staging of the fold
+        lines += [
+            "    const int rs_rank = rs_j0 / RS_PER_RANK, rs_jl = rs_j0 - rs_rank * RS_PER_RANK;",
+        ]
+    for k, (buf, a) in enumerate(s_list):
+        src = (f"reinterpret_cast<const float*>(rs_peer[{k} * RS_RANKS + rs_rank])[{a} * rs_jl + rs_e]" if peer
+               else f"{buf}[{a} * rs_j0 + rs_e]")
         lines += [
             "#pragma unroll 4",
             f"    for (int rs_e = rs_l; rs_e < rs_jn * {a}; rs_e += 32)",
-            f"      rs_s[(rs_e / {a}) * {rec} + {offsets[buf]} + rs_e % {a}] = {buf}[{a} * rs_j0 + rs_e];",
+            f"      rs_s[(rs_e / {a}) * {rec} + {offsets[buf]} + rs_e % {a}] = {src};",
         ]
     lines += [
         "    __syncwarp();",
@@ -342,10 +360,13 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "per_block": 32 * RB,
         "block": nthreads,
         "split": split,
+        **({"peer_ranks": peer, "peer_streams": [b for b, _a in s_list],
+            "extra_args": [{"kind": "peer_table"}]} if peer else {}),
         "fmad": True,
         "order": ("preserved-fold" if split == 1 else f"{split} contiguous source chunks, added in chunk order")
         + ", fast-math",
-        "pre": [],
+        "pre": ([f"({py_expr(NS)}) % {peer} == 0", f"(({py_expr(NS)}) // {peer}) % {JT} == 0",
+                 f"(({py_expr(NS)}) // {split}) % {JT} == 0", f"({py_expr(NS)}) % {split} == 0"] if peer else []),
     }
     return "\n".join(lines) + "\n", plan
 

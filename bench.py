@@ -703,9 +703,14 @@ def _roofline(wl, achieved, peaks, args):
             traffic = json.loads(summary.read_text()).get("dram_bytes_per_launch")
         except Exception:  # noqa: BLE001
             traffic = None
-    return {"bound": wl.bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
-            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": src,
-            "algorithmic_work_per_launch": wl.work()}
+    out = {"bound": wl.bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
+           "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": src,
+           "algorithmic_work_per_launch": wl.work()}
+    if wl.bound == "tensor":
+        # context: B200_PROFILING.md's nominal dense TF32 (1.1 PFLOP/s) / 3
+        out["nominal_peak"] = round(1100e3 / 3.0, 3)
+        out["frac_of_nominal"] = round(achieved / (1100e3 / 3.0), 4)
+    return out
 
 
 def _tf32_peak():

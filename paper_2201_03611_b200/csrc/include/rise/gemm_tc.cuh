@@ -258,6 +258,20 @@ RS_DEVICE void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// 16-byte async-proxy copy into the peer CTA's shared memory whose
+// completion is a complete_tx on the peer's mbarrier: the cross-CTA "stage
+// converted" signal.  The copy is issued after fence.proxy.async + a barrier
+// of the converting threads and its complete_tx has release semantics, so
+// it orders those threads' shared-memory writes before the peer's MMA reads
+// (an acquire wait) without a cluster-scope MEMBAR in the instruction stream.
+RS_DEVICE void signal_s2s_cluster(unsigned dst_cluster_addr, const void* src, unsigned bar_cluster_addr) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];" ::"r"(
+          dst_cluster_addr),
+      "r"(rs_smem_addr(src)), "r"(bar_cluster_addr)
+      : "memory");
+}
+
 RS_DEVICE void mbar_arrive_remote(unsigned cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
@@ -344,6 +358,8 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
   unsigned long long* empty = bars + 2 * STAGES;
   unsigned long long* tmem_full = bars + 3 * STAGES;
   unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 3 * STAGES + 1);
+  // 16-byte landing slot of the CTA-1 -> CTA-0 "stage converted" signal copies
+  unsigned char* sig_slot = reinterpret_cast<unsigned char*>(bars) + ((3 * STAGES + 2) * 8 + 15) / 16 * 16;
 
   constexpr int KB = K / BK;
   constexpr int NTN = N / BN;
@@ -367,7 +383,9 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
     rs_tmap_prefetch(mapB);
     for (int s = 0; s < STAGES; ++s) {
       rs_mbar_init(&full[s], 1);
-      rs_mbar_init(&conv[s], 2);  // one arrival from each CTA of the pair
+      // phase = CTA 0's converters (one arrival, +16 tx expected) and CTA 1's
+      // signal copy (complete_tx 16 bytes), in either order
+      rs_mbar_init(&conv[s], 1);
       rs_mbar_init(&empty[s], 1);
     }
     rs_mbar_init(tmem_full, 1);
@@ -421,10 +439,15 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
       rs_mbar_wait(&full[s], ph);
       split_tile<false>(a_raw(s), a_lo(s), G::TILE_A, t);
       split_tile<false>(b_raw(s), b_lo(s), G::TILE_B, t);
-      rs_fence_proxy_async();
-      // one cluster-scope release per CTA and stage (its fence is the costly part)
+      rs_fence_proxy_async();  // this thread's tile writes precede later async-proxy reads
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (t == 0) mbar_arrive_remote(mapa(rs_smem_addr(&conv[s]), 0u));
+      if (t == 0) {
+        if (rank == 0) {
+          rs_mbar_arrive_expect_tx(&conv[s], 16u);  // the MMA issuer is in this CTA: CTA-scope release
+        } else {
+          signal_s2s_cluster(mapa(rs_smem_addr(sig_slot), 0u), sig_slot, mapa(rs_smem_addr(&conv[s]), 0u));
+        }
+      }
     }
     rs_mbar_wait(tmem_full, 0u);
     fence_after();

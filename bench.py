@@ -218,6 +218,25 @@ class Sgemm(Workload):
                 "sample": f"{rows} rows of the 4096^3 sgemm, the reference's emitted OpenMP C (oracle/_ref)"}
 
 
+class SgemmNN(Sgemm):
+    key = "sgemm_nn"
+    program = ("A |> mapGlobal(arow => transpose(B) |> mapGlobal(bcol => zip |> reduceSeq)) (programs.SGEMM; "
+               "B row-major, MN-major tensor-core operand)")
+
+    def compile(self):
+        from paper_2201_03611_b200 import compile_program, programs
+
+        return compile_program(programs.SGEMM, None, name="sgemm"), {"n": self.n, "m": self.m, "k": self.k}
+
+    def inputs(self):
+        A, Bt = super().inputs()
+        return [A, np.ascontiguousarray(Bt.T)]
+
+    def cpu_sample(self, host):
+        A, B = host
+        return super().cpu_sample([A, np.ascontiguousarray(B.T)])  # the reference C takes Bt
+
+
 class Nbody(Workload):
     key = "nbody"
     program = "all-pairs map/reduce + Euler velocity step (programs.NBODY)"
@@ -257,7 +276,7 @@ class Nbody(Workload):
                 "kind": kind, "sample": f"{count} target bodies x {self.n} sources, {what}"}
 
 
-WORKLOADS = {w.key: w for w in (Gemv, GemvOpt, Dot, DotChunked, Conv, Sgemm, Nbody)}
+WORKLOADS = {w.key: w for w in (Gemv, GemvOpt, Dot, DotChunked, Conv, Sgemm, SgemmNN, Nbody)}
 
 
 def _best_of(fn, k):
@@ -512,6 +531,7 @@ def _parallelism_text(wl, world):
         "gemv": f"weak: rank r owns an 8192-row band of an ({world}x8192) x 8192 matrix, x replicated, y sharded",
         "gemv_opt": f"weak: rank r owns an 8192-row band of an ({world}x8192) x 8192 matrix, x replicated",
         "sgemm": f"weak: rank r owns a 4096-row block of A ({world}x4096 rows), B replicated",
+        "sgemm_nn": f"weak: rank r owns a 4096-row block of A ({world}x4096 rows), B replicated",
         "dot": "weak: rank r owns a 2^24 chunk; partials all-gathered (rs_allgather, NCCL) and folded in rank order",
         "dot_chunked": "weak: rank r owns a 2^24 chunk; partials all-gathered (rs_allgather, NCCL), rank-order fold",
         "conv": "weak: rank r owns an 8192-row band; halo rows pulled from the neighbours' bands over NVLink "

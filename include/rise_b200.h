@@ -130,7 +130,8 @@ int rs_event_elapsed_ms(float* ms, void* start, void* end);
 /* Encode a 2-D (inner dim0, outer dim1) tiled TMA descriptor for fp32 data
  * into the 128-byte buffer `desc` (CUtensorMap layout).  `row_stride_bytes`
  * is the byte distance between consecutive dim1 rows (multiple of 16).
- * `swizzle`: 0 none, 1 32B, 2 64B, 3 128B.  Out-of-bounds box elements are
+ * `swizzle`: 0 none, 1 32B, 2 64B, 3 128B, 4 128B with 32-byte atoms (the
+ * layout tcgen05 reads MN-major tf32 operands in).  Out-of-bounds box elements are
  * zero-filled by the hardware. */
 int rs_tma_desc_2d_f32(void* desc, const void* base,
                        uint64_t dim0, uint64_t dim1, uint64_t row_stride_bytes,

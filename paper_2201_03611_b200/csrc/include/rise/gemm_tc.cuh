@@ -320,6 +320,21 @@ RS_DEVICE void tmem_dealloc2(unsigned taddr) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(COLS) : "memory");
 }
 
+// MN-major variant (B stored K x N, row-major).  MN-major tf32 operands
+// only exist in the 128-byte swizzle with 32-byte atomicity (UMMA layout
+// type 1, SWIZZLE_128B_BASE32B; the TMA map uses
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): atoms of 4 K-rows x 32 N-values
+// (512 B); consecutive 32-column N groups are LBO = 4 KiB apart (one 32 x 32
+// TMA box each), K atoms SBO = 512 B apart.
+RS_DEVICE unsigned long long smem_desc_mn(unsigned saddr) {
+  unsigned long long d = (unsigned long long)((saddr >> 4) & 0x3FFFu);
+  d |= (unsigned long long)(4096 >> 4) << 16;
+  d |= (unsigned long long)(512 >> 4) << 32;
+  d |= 1ull << 46;
+  d |= 1ull << 61;
+  return d;
+}
+
 template <int BN_, int STAGES_>
 struct Cfg2 {
   static constexpr int BN = BN_;  // pair tile: 256 x BN; each CTA stages BN/2 rows of Bt
@@ -333,6 +348,7 @@ struct Cfg2 {
       (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(256 >> 4) << 24);
   static constexpr unsigned IDESC_HALF =
       (1u << 4) | (2u << 7) | (2u << 10) | (unsigned((BN / 2) >> 3) << 17) | (unsigned(256 >> 4) << 24);
+  static constexpr unsigned IDESC_BMN = IDESC | (1u << 16);  // b_major = MN
 };
 
 // blockIdx.x = 2 * pair + rank.  Tiles 256 x BN in (tm, tn) order, tn
@@ -345,7 +361,7 @@ struct Cfg2 {
 // is resident at once (the split is only used when the units fit in one
 // wave), the second half never waits, and the order of the final add is
 // fixed: deterministic.
-template <int M, int N, int K, int BN, int STAGES>
+template <int M, int N, int K, int BN, int STAGES, bool B_MN = false>
 RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* mapA, const rs_tmap* mapB,
                                int n_full, float* __restrict__ ws, unsigned* __restrict__ flags) {
   using G = Cfg2<BN, STAGES>;
@@ -405,7 +421,13 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
         rs_mbar_wait(&empty[s], ph ^ 1u);
         rs_mbar_arrive_expect_tx(&full[s], G::TILE_A + G::TILE_B);
         rs_tma_load_2d(a_raw(s), mapA, kb * BK, m0 + 128 * (int)rank, &full[s]);
-        rs_tma_load_2d(b_raw(s), mapB, kb * BK, n0 + (BN / 2) * (int)rank, &full[s]);
+        if (B_MN) {  // BN/2 columns of K x N B as 32 x 32 boxes, 4 KiB apart
+#pragma unroll
+          for (int b = 0; b < BN / 64; ++b)
+            rs_tma_load_2d(b_raw(s) + b * 4096, mapB, n0 + (BN / 2) * (int)rank + 32 * b, kb * BK, &full[s]);
+        } else {
+          rs_tma_load_2d(b_raw(s), mapB, kb * BK, n0 + (BN / 2) * (int)rank, &full[s]);
+        }
       }
     }
   } else if (warp == 1) {
@@ -417,14 +439,20 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
         fence_after();
         const unsigned long long ahi = smem_desc(rs_smem_addr(a_raw(s)));
         const unsigned long long alo = smem_desc(rs_smem_addr(a_lo(s)));
-        const unsigned long long bhi = smem_desc(rs_smem_addr(b_raw(s)));
-        const unsigned long long blo = smem_desc(rs_smem_addr(b_lo(s)));
+        const unsigned long long bhi =
+            B_MN ? smem_desc_mn(rs_smem_addr(b_raw(s))) : smem_desc(rs_smem_addr(b_raw(s)));
+        const unsigned long long blo =
+            B_MN ? smem_desc_mn(rs_smem_addr(b_lo(s))) : smem_desc(rs_smem_addr(b_lo(s)));
+        constexpr unsigned idesc = B_MN ? G::IDESC_BMN : G::IDESC;
 #pragma unroll
         for (int k = 0; k < BK / 8; ++k) {
+          // K-major: the next 8 K values are 32 bytes along the swizzled row;
+          // MN-major: the next 8 K rows are the next 1 KiB atom
           const unsigned long long off = (unsigned long long)(k * 32) >> 4;
-          mma2(tmem, alo + off, bhi + off, G::IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
-          mma2(tmem, ahi + off, blo + off, G::IDESC, 1u);
-          mma2(tmem, ahi + off, bhi + off, G::IDESC, 1u);
+          const unsigned long long boff = B_MN ? (unsigned long long)(k * 1024) >> 4 : off;
+          mma2(tmem, alo + off, bhi + boff, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+          mma2(tmem, ahi + off, blo + boff, idesc, 1u);
+          mma2(tmem, ahi + off, bhi + boff, idesc, 1u);
         }
         commit2_multicast(&empty[s]);
       }

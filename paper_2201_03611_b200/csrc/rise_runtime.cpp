@@ -530,6 +530,7 @@ int rs_tma_desc_2d_f32(void* desc, const void* base, uint64_t dim0, uint64_t dim
   if (swizzle == 1) sw = CU_TENSOR_MAP_SWIZZLE_32B;
   if (swizzle == 2) sw = CU_TENSOR_MAP_SWIZZLE_64B;
   if (swizzle == 3) sw = CU_TENSOR_MAP_SWIZZLE_128B;
+  if (swizzle == 4) sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;  // MN-major tf32 UMMA operands
   CU(g_drv.TensorMapEncodeTiled((CUtensorMap*)desc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base),
                                 dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),

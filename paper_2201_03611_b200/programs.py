@@ -98,6 +98,15 @@ def nbody = depFun((n: Nat) =>
                    |> fun(r2 => rsqrt(r2) * rsqrt(r2) * rsqrt(r2)))) ))(0.0f)) )) )) ))))
 """
 
+# C4 without the pre-transposed operand: B is K x N row-major, read through
+# the extension's transpose (the tensor-core template takes it MN-major)
+SGEMM = """\
+def sgemm = depFun((n: Nat, m: Nat, k: Nat) =>
+  fun(A: Array[n, Array[k, f32]] => fun(B: Array[k, Array[m, f32]] =>
+    A |> mapGlobal(fun(arow => transpose(B) |> mapGlobal(fun(bcol =>
+      zip(arow)(bcol) |> reduceSeq(Private)(fun(acc, p => acc + fst(p) * snd(p)))(0.0f) ))) ))))
+"""
+
 # the same step for a block of t target bodies against all n sources (the
 # per-GPU program of the multi-GPU decomposition, shard.sharded_nbody)
 NBODY_SHARD = """\

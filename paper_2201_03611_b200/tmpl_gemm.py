@@ -57,10 +57,18 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
     def is_row(ld, var):
         return nat.equal(ld.index, nat.normalize(V(var) * K + V(p)), prog.assumptions)
 
+    def is_col(ld, var):  # B[k][j] of a row-major K x N matrix (e.g. read through transpose(B))
+        return nat.equal(ld.index, nat.normalize(V(p) * N + V(var)), prog.assumptions)
+
+    b_mn = False  # B is MN-major in shared memory (UMMA b_major = 1)
     if is_row(x, iv) and is_row(y, jv):
         a_ld, b_ld = x, y
     elif is_row(y, iv) and is_row(x, jv):
         a_ld, b_ld = y, x
+    elif PAIR and is_row(x, iv) and is_col(y, jv):
+        a_ld, b_ld, b_mn = x, y, True
+    elif PAIR and is_row(y, iv) and is_col(x, jv):
+        a_ld, b_ld, b_mn = y, x, True
     else:
         return None
     for ld in (a_ld, b_ld):
@@ -81,7 +89,8 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
     lines = kernel_head(prog, name, temps, launch_bounds="192, 1", extra_params=extra)
     if PAIR:
         lines += [
-            f"  rise_gemm::gemm_3xtf32_2sm<{r(M)}, {r(N)}, {r(K)}, {PAIR_BN}, {PAIR_STAGES}>"
+            f"  rise_gemm::gemm_3xtf32_2sm<{r(M)}, {r(N)}, {r(K)}, {PAIR_BN}, {PAIR_STAGES}, "
+            f"{'true' if b_mn else 'false'}>"
             f"({st.target.buf}, {r(N)}, &rs_mapA, &rs_mapB, rs_nfull, rs_ws, rs_flags);",
             "}",
         ]
@@ -93,6 +102,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
             "K": py_expr(K),
             "bn": PAIR_BN,
             "pair": True,
+            "b_major": "mn" if b_mn else "k",
             "fmad": False,
             "order": "3xtf32 tensor-core, CTA pairs; tail tiles K-split in two halves (reassociated)",
             "pre": [f"({py_expr(M)}) % 256 == 0", f"({py_expr(N)}) % {PAIR_BN} == 0", f"({py_expr(K)}) % 32 == 0",
@@ -101,8 +111,10 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
             "extra_args": [
                 {"kind": "tma2d", "buf": a_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(M)],
                  "pitch": py_expr(K), "box": [32, 128], "swizzle": 3},
-                {"kind": "tma2d", "buf": b_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(N)],
-                 "pitch": py_expr(K), "box": [32, PAIR_BN // 2], "swizzle": 3},
+                ({"kind": "tma2d", "buf": b_ld.buf, "offset": "0", "dims": [py_expr(N), py_expr(K)],
+                  "pitch": py_expr(N), "box": [32, 32], "swizzle": 4} if b_mn else
+                 {"kind": "tma2d", "buf": b_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(N)],
+                  "pitch": py_expr(K), "box": [32, PAIR_BN // 2], "swizzle": 3}),
                 {"kind": "gemm_full_tiles", "M": py_expr(M), "N": py_expr(N), "K": py_expr(K), "bn": PAIR_BN},
                 {"kind": "workspace", "name": f"rs_ws_{base_name}_ktail"},
                 {"kind": "workspace", "name": f"rs_ws_{base_name}_kflags"},

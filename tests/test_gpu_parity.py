@@ -228,6 +228,23 @@ def test_sgemm_k_split_tail_tiles(gpu, n, m, k, monkeypatch):
     np.testing.assert_array_equal(got[:256], whole[:256])
 
 
+@pytest.mark.parametrize("n,m,k", [(256, 512, 512), (512, 768, 96), (4096, 4096, 4096)])
+def test_sgemm_transpose_b_mn_major_within_bound(gpu, n, m, k):
+    """C = A x B with B row-major (read through transpose): the tcgen05
+    template takes B MN-major (UMMA b_major = 1, 32 x 32 TMA boxes)."""
+    c = compile_program(programs.SGEMM, None, name="sgemm")
+    code = emit_cuda(c.unit)
+    assert code.plan["stages"][0]["kind"] == "gemm_tc" and code.plan["stages"][0]["b_major"] == "mn"
+    A = oracle.rng_inputs(4, n, k)
+    B = oracle.rng_inputs(24, k, m)
+    got = run_cuda(code, c.unit, {"n": n, "m": m, "k": k}, [A, B], as_numpy=True).reshape(n, m)
+    rows = slice(max(0, n - 256), n)
+    C64, absC = oracle.sgemm_bt_f64(A[rows], np.ascontiguousarray(B.T))
+    err = np.abs(got[rows] - C64)
+    assert np.all(err <= oracle.gemm_bound(k, absC)), float(np.max(err / (absC * oracle.U * k)))
+    assert float(np.max(err / absC)) < 1e-5
+
+
 def test_sgemm_generic_exact_bit_exact(gpu):
     c = compile_program(programs.SGEMM_BT, None, name="sgemm")
     code = emit_cuda(c.unit, idioms=False)

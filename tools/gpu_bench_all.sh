@@ -4,7 +4,7 @@
 mkdir -p gpurun_out/bench
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-for w in ${WORKLOADS:-gemv gemv_opt dot dot_chunked conv sgemm nbody}; do
+for w in ${WORKLOADS:-gemv gemv_opt dot dot_chunked conv sgemm sgemm_nn nbody}; do
   timeout 600 python bench.py --workload $w --steps ${STEPS:-50} --warmup 5 > gpurun_out/bench/bench_$w.json 2> gpurun_out/bench/bench_$w.err
   timeout 600 python bench.py --impl reference --workload $w --steps 3 --warmup 3 > gpurun_out/bench/ref_$w.json 2> gpurun_out/bench/ref_$w.err
 done

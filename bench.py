@@ -146,6 +146,17 @@ class DotChunked(Dot):
         c = compile_program(programs.DOT, gpu_rules.CHUNKED_REDUCE_STRATEGY, name="dotChunked")
         return c, {"n": self.n}
 
+    def cpu_sample(self, host):
+        import oracle
+
+        if oracle.ref_lib() is None:
+            return super().cpu_sample(host)
+        a, b = host
+        t = _best_of(lambda: oracle.ref_dot_chunked(a, b), 3)
+        return {"value": self.work() / t / 1e9, "unit": "GB/s", "cores": oracle.threads(), "kind": "reference",
+                "sample": ("full 2^24 dot, the reference's emitted OpenMP C of the same chunked schedule "
+                           "(chunks in parallel, then the fold of the partials), best of 3")}
+
 
 class Conv(Workload):
     key = "conv"

@@ -71,6 +71,7 @@ def ref_lib():
         L.sgemmBtKernel.argtypes = [_fp, _int, _int, _int, _fp, _fp]
         L.convKernel.argtypes = [_fp, _int, _int, _fp, _fp]
         L.asumKernel.argtypes = [_fp, _int, _fp]
+        L.dotChunkedKernel.argtypes = [_fp, _int, _fp, _fp]
         L.nbodyShardKernel.argtypes = [_fp, _int, _int, _fp, _fp, _fp, _fp]
         _ref = L
     return _ref
@@ -173,6 +174,16 @@ def ref_mv(M, x, s=None):
     else:
         L.mvOptKernel(_ptr(out), n, m, s, _ptr(M), _ptr(x))
     return out
+
+
+def ref_dot_chunked(a, b):
+    """The reference emitter's OpenMP C for DOT + the chunked-reduce strategy:
+    4096-element chunk folds in parallel, then their left fold."""
+    L = ref_lib()
+    a, b = f32(a), f32(b)
+    out = np.zeros(1, np.float32)
+    L.dotChunkedKernel(_ptr(out), a.size, _ptr(a), _ptr(b))
+    return out[0]
 
 
 def ref_asum(x):

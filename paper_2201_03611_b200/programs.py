@@ -46,6 +46,8 @@ depFun((n: Nat) => fun(a: Array[n, f32] => fun(b: Array[n, f32] =>
     |> reduceSeq(Private)(fun(acc, v => acc + v))(0.0f) )))
 """
 DOT_CHUNK = 4096
+# ... and the same schedule derived from DOT by the GPU rewrite rules
+from .gpu_rules import CHUNKED_REDUCE_STRATEGY as DOT_CHUNKED_STRATEGY  # noqa: E402
 
 MV = """\
 // matrix-vector multiplication: for each row, a dot product with x

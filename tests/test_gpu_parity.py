@@ -321,6 +321,8 @@ def test_dot_chunked_program_bit_exact(gpu, n):
     ch = programs.DOT_CHUNK
     partials = np.array([oracle.dot(a[i:i + ch], b[i:i + ch]) for i in range(0, n, ch)], np.float32)
     assert got == oracle.dot(partials, np.ones_like(partials))
+    if oracle.ref_lib() is not None:  # the reference's own OpenMP emission of the same schedule
+        assert np.float32(got).view(np.uint32) == np.float32(oracle.ref_dot_chunked(a, b)).view(np.uint32)
 
 
 @pytest.mark.parametrize("n", [1 << 16, 1000, 3])

@@ -124,6 +124,15 @@ def test_reference_c_asum_is_the_sequential_fold():
     assert oracle.ref_asum(x).view(np.uint32) == np.float32(want).view(np.uint32)
 
 
+@needs_ref
+def test_reference_c_chunked_dot_is_the_chunked_fold():
+    a = oracle.rng_inputs(1, 1 << 20)
+    b = oracle.rng_inputs(2, 1 << 20)
+    parts = np.array([oracle.dot(a[i:i + 4096], b[i:i + 4096]) for i in range(0, 1 << 20, 4096)], np.float32)
+    want = oracle.dot(parts, np.ones_like(parts))
+    assert np.float32(oracle.ref_dot_chunked(a, b)).view(np.uint32) == np.float32(want).view(np.uint32)
+
+
 def test_left_fold_order_is_pinned():
     # interpreter.py:134-138: reduce is a left fold from init; 0.1+0.2+0.3 in
     # fp32 (test_interpreter.py:79-84) — the restatement does the same

@@ -393,6 +393,13 @@ def run_ours(args, rank, world, local_rank):
     out = torch.empty(exe.output_size, dtype=torch.float32, device="cuda")
     extra = {}
     peer_sources = None
+    if exe.plan.get("peer_halo"):
+        from paper_2201_03611_b200 import shard
+
+        torch.cuda.synchronize()
+        peer_sources = shard.PeerHaloRows(dev_in[0].view(nats["n"], nats["m"]), exe.plan["stages"][0]["halo_rows"])
+        dist.barrier()
+        extra.update(peer_sources.extra)
     if exe.plan.get("peer_ranks"):
         from paper_2201_03611_b200 import shard
 
@@ -545,8 +552,10 @@ def _parallelism_text(wl, world):
         "sgemm_nn": f"weak: rank r owns a 4096-row block of A ({world}x4096 rows), B replicated",
         "dot": "weak: rank r owns a 2^24 chunk; partials all-gathered (rs_allgather, NCCL) and folded in rank order",
         "dot_chunked": "weak: rank r owns a 2^24 chunk; partials all-gathered (rs_allgather, NCCL), rank-order fold",
-        "conv": "weak: rank r owns an 8192-row band; halo rows pulled from the neighbours' bands over NVLink "
-                "(rs_halo_exchange, CUDA IPC) per step",
+        "conv": ("weak: rank r owns an 8192-row band; " + (
+            "the stencil kernel reads the neighbours' edge rows in place over NVLink (peer pointers, "
+            "halo exchange fused into the border-tile staging)" if _conv_fused_halo() else
+            "halo rows pulled from the neighbours' bands over NVLink (rs_halo_exchange, CUDA IPC) per step")),
         "nbody": (f"strong: 131072 bodies, {131072 // world} targets per rank; "
                   + ("every rank's position/mass block read in place over NVLink by the force kernel "
                      "(peer pointers, all-gather fused into the fold)" if _nbody_peer() else
@@ -559,6 +568,11 @@ def _distributed_variant(wl, compiled, nats, host, rank, world):
     (paper_2201_03611_b200/shard.py)."""
     from paper_2201_03611_b200 import compile_program, programs
 
+    if wl.key == "conv" and _conv_fused_halo():
+        # the fused variant: the stencil kernel reads its neighbours' edge rows
+        # in place (peer pointers), so the band is exactly this rank's rows
+        wl.emit_kwargs = {"peer_halo": True}
+        return compiled, nats, host
     if wl.key == "conv":
         img, w = host
         local = np.empty((img.shape[0] + 2, img.shape[1]), np.float32)
@@ -588,6 +602,10 @@ def _distributed_variant(wl, compiled, nats, host, rank, world):
 
 def _nbody_peer():
     return os.environ.get("RISE_NBODY_PEER", "1") == "1"
+
+
+def _conv_fused_halo():
+    return os.environ.get("RISE_CONV_FUSED_HALO", "1") == "1"
 
 
 def _bound_launch(exe, dev_in, out, stream, extra=None):

@@ -478,7 +478,7 @@ def arg_names(prog: lir.Program, temps):
 # whole units
 
 
-def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0) -> CudaCode:
+def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, peer_halo=False) -> CudaCode:
     """Emit the sm100a kernel text (and launch plan) for an ImperativeUnit.
 
     `reassociate=False` keeps every reduction in the program's own order
@@ -489,11 +489,18 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0) -> 
     `peer_ranks=R` (multi-GPU, one process per GPU): the `allpairs` source
     streams are distributed over R ranks in equal contiguous blocks and read
     in place through a device table of peer pointers (extra launch argument
-    `rs_peer_table`), fusing the all-gather of the sources into the fold."""
+    `rs_peer_table`), fusing the all-gather of the sources into the fold.
+
+    `peer_halo=True` (multi-GPU row bands): the `stencil2d` template reads
+    the rows padClamp would invent above / below the band from the
+    neighbours' bands in place (extra launch arguments `rs_halo_top` /
+    `rs_halo_bot`: peer pointers to their edge rows, or NULL at the image's
+    real edges), fusing the halo exchange into the stencil."""
     from . import idioms as idiom_mod
 
     prog = lir.build(unit)
     prog.peer_ranks = int(peer_ranks)
+    prog.peer_halo = bool(peer_halo)
     stages, temps = split_stages(prog.body, prog)
     kernels = []
     plan_stages = []
@@ -506,6 +513,8 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0) -> 
         match = idiom_mod.match(prog, st, base, temps, exact, reassociate) if idioms else None
         if peer_ranks and (match is None or not match.plan.get("peer_ranks")):
             raise EmitError("peer_ranks needs a stage the allpairs template takes (sources read in place)")
+        if peer_halo and (match is None or not match.plan.get("peer_halo")):
+            raise EmitError("peer_halo needs a stage the stencil2d template takes (halo rows read in place)")
         if match is not None:
             kernels.append(match.text)
             for inc in match.includes:
@@ -527,6 +536,8 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0) -> 
         "exact": exact,
         "reassociate": reassociate,
     }
+    if peer_halo:
+        plan["peer_halo"] = True
     if peer_ranks:
         plan["peer_ranks"] = int(peer_ranks)
         peers = {b for st in plan_stages for b in st.get("peer_streams", [])}

@@ -172,6 +172,7 @@ class Program:
     clamps: dict = field(default_factory=dict)  # "__clampK" -> (inner Nat, hi Nat)
     names: dict = field(default_factory=dict)  # DPIA name -> C name
     peer_ranks: int = 0  # emission option: allpairs sources read from R ranks' blocks
+    peer_halo: bool = False  # emission option: stencil halo rows read from the neighbours' bands
 
 
 # ---------------------------------------------------------------------------

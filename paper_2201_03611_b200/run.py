@@ -69,9 +69,9 @@ class Executable:
         for st in self.plan["stages"]:
             chosen = st
             if st.get("pre") and not all(eval_py(p, self.nats) for p in st["pre"]):
-                if st.get("peer_ranks"):
-                    raise InterpreterError(f"{st['name']}: sizes {self.nats} do not split over "
-                                           f"{st['peer_ranks']} ranks' source blocks (no fallback reads peers)")
+                if st.get("peer_ranks") or st.get("peer_halo"):
+                    raise InterpreterError(f"{st['name']}: sizes {self.nats} fail the peer-memory variant's "
+                                           f"preconditions {st['pre']} (no fallback reads peers)")
                 chosen = st["fallback"]
             fmad = fmad or bool(chosen.get("fmad", False))
             name_expr = f"{chosen['name']}<{targs}>" if targs else chosen["name"]
@@ -194,6 +194,9 @@ class Executable:
             pitch = eval_py(extra.get("pitch", extra["dims"][0]), self.nats)
             return rt.tma_desc_2d_f32(base, dims[0], dims[1], pitch * 4, extra["box"][0], extra["box"][1],
                                       extra.get("swizzle", 0))
+        if kind == "peer_ptr":  # optional: absent / None / 0 -> NULL (e.g. the image's real edge)
+            value = buffers.get(extra["name"])
+            return ctypes.c_void_p(0 if value is None else _dptr(value) if hasattr(value, "data_ptr") else int(value))
         if kind == "peer_table":
             table = buffers.get("rs_peer_table")
             if table is None:

@@ -214,3 +214,49 @@ class PeerSources:
         for p in self.opened:
             runtime.ipc_close(p)
         self.opened = []
+
+
+class PeerHaloRows:
+    """The halo rows of a `stencil2d` kernel emitted with peer_halo=True:
+    each rank maps its neighbours' bands (CUDA IPC) once and hands the
+    kernel pointers to the rows it reads in place — the last `above` rows
+    of the band above and the first `below` rows of the band below (plan
+    stage `halo_rows`); at the image's real edges the pointer is NULL and
+    the kernel clamps (padClamp2D).  `band` is this rank's [rows, m] device
+    tensor (no halo rows of its own)."""
+
+    def __init__(self, band, halo_rows, group=None):
+        import torch.distributed as dist
+
+        from . import runtime
+
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        rows, m = band.shape
+        esize = band.element_size()
+        handle, off = runtime.ipc_handle(band.data_ptr())
+        peers = [None] * self.world
+        dist.all_gather_object(peers, (handle, off, rows), group=group)
+        ht, hb = halo_rows
+        self.opened = []
+        self.extra = {"rs_halo_top": 0, "rs_halo_bot": 0}
+        if self.rank > 0:
+            h, o, r = peers[self.rank - 1]
+            if r < ht:
+                raise ValueError(f"the band above has {r} rows; the stencil needs {ht}")
+            p = runtime.ipc_open(h, o)
+            self.opened.append(p)
+            self.extra["rs_halo_top"] = p + (r - ht) * m * esize
+        if self.rank < self.world - 1:
+            h, o, r = peers[self.rank + 1]
+            if r < hb:
+                raise ValueError(f"the band below has {r} rows; the stencil needs {hb}")
+            p = runtime.ipc_open(h, o)
+            self.opened.append(p)
+            self.extra["rs_halo_bot"] = p
+
+    def close(self):
+        from . import runtime
+
+        for p in self.opened:
+            runtime.ipc_close(p)
+        self.opened = []

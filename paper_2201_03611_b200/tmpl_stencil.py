@@ -163,6 +163,26 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     params = ["const __grid_constant__ rs_tmap rs_map"]
     if tma_store:
         params.append("const __grid_constant__ rs_tmap rs_omap")
+    peer_halo = bool(getattr(prog, "peer_halo", False))
+    ht, hb = -o0lo, o0hi  # rows of halo above / below the band
+    row_pass = [
+        "        if (rs_y < rs_ylo) rs_tile[rs_e] = rs_tile[rs_ylo * RS_SW + rs_x];",
+        "        else if (rs_y > rs_yhi) rs_tile[rs_e] = rs_tile[rs_yhi * RS_SW + rs_x];",
+    ]
+    if peer_halo:
+        # multi-GPU row bands: the rows padClamp would invent above / below
+        # this band are the neighbours' edge rows, read in place (peer
+        # pointers over NVLink; NULL at the image's real edges = clamp) —
+        # the halo exchange fused into the stencil's border-tile staging
+        params += ["const float* __restrict__ rs_halo_top", "const float* __restrict__ rs_halo_bot"]
+        row_pass = [
+            "        const int rs_gc = rs_tc0 + rs_x;  // image column of the cell",
+            "        const bool rs_cin = rs_gc >= 0 && rs_gc < RS_W;",
+            "        if (rs_y < rs_ylo) rs_tile[rs_e] = rs_halo_top != nullptr && rs_cin",
+            f"            ? rs_halo_top[(rs_tr0 + rs_y + {ht}) * RS_W + rs_gc] : rs_tile[rs_ylo * RS_SW + rs_x];",
+            "        else if (rs_y > rs_yhi) rs_tile[rs_e] = rs_halo_bot != nullptr && rs_cin",
+            "            ? rs_halo_bot[(rs_tr0 + rs_y - RS_H) * RS_W + rs_gc] : rs_tile[rs_yhi * RS_SW + rs_x];",
+        ]
     lines = kernel_head(prog, name, temps, launch_bounds=f"{TX * TY}, {BLOCKS_PER_SM}", extra_params=params)
     lines += [
         f"  constexpr int RS_R = {r(R)}, RS_C = {r(C)};",
@@ -228,8 +248,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "      // rows first (full width), then columns: corner cells end up clamped in both dimensions",
         f"      for (int rs_e = rs_tid; rs_e < RS_SR * RS_SW; rs_e += {TX * TY}) {{",
         "        const int rs_y = rs_e / RS_SW, rs_x = rs_e - rs_y * RS_SW;",
-        "        if (rs_y < rs_ylo) rs_tile[rs_e] = rs_tile[rs_ylo * RS_SW + rs_x];",
-        "        else if (rs_y > rs_yhi) rs_tile[rs_e] = rs_tile[rs_yhi * RS_SW + rs_x];",
+        *row_pass,
         "      }",
         "      __syncthreads();",
         f"      for (int rs_e = rs_tid; rs_e < RS_SR * RS_SW; rs_e += {TX * TY}) {{",
@@ -308,6 +327,10 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
                                    "dims": [py_expr(C), py_expr(R)], "pitch": py_expr(row_coef),
                                    "box": [TC, TR], "swizzle": 0})
         plan["tma_store"] = True
+    if peer_halo:  # (kernel parameter order: rs_map, [rs_omap], rs_halo_top, rs_halo_bot)
+        plan["peer_halo"] = True
+        plan["halo_rows"] = [ht, hb]
+        plan["extra_args"] += [{"kind": "peer_ptr", "name": "rs_halo_top"}, {"kind": "peer_ptr", "name": "rs_halo_bot"}]
     return "\n".join(lines) + "\n", plan
 
 

@@ -31,11 +31,13 @@ from . import lir
 from ._ref import nat
 from .emit_cuda import GenericKernel, NatRenderer, Stage, ValueRenderer, kernel_head, py_expr
 
-TX, TY = 32, 8
-RPT = 8  # output rows per thread
+import os  # noqa: E402
+
+TX = 32  # threads along a row (one warp: 16-byte stores of adjacent columns)
+TY = int(os.environ.get("RISE_STENCIL_TY", "8"))
+RPT = int(os.environ.get("RISE_STENCIL_RPT", "8"))  # output rows per thread
 CPT = 4  # adjacent output columns per thread
 TR, TC = TY * RPT, TX * CPT
-import os  # noqa: E402
 
 # persistent blocks per SM (each holds two 36 KB stages); overridable for sweeps
 BLOCKS_PER_SM = int(os.environ.get("RISE_STENCIL_BPS", "3"))

@@ -377,8 +377,11 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
   // 16-byte landing slot of the CTA-1 -> CTA-0 "stage converted" signal copies
   unsigned char* sig_slot = reinterpret_cast<unsigned char*>(bars) + ((3 * STAGES + 2) * 8 + 15) / 16 * 16;
 
-  constexpr int KB = K / BK;
-  constexpr int NTN = N / BN;
+  // ragged shapes: the TMA unit zero-fills the parts of the edge tiles
+  // outside A / B (a zero K tail adds nothing), and the epilogue stores only
+  // in-range rows and columns
+  constexpr int KB = (K + BK - 1) / BK;
+  constexpr int NTN = (N + BN - 1) / BN;
   const unsigned rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1;
   const bool split = pair >= n_full;
@@ -482,7 +485,21 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int trow = 128 * (int)rank + row;  // row within the 256-row pair tile
-    float* crow = C + (long long)(m0 + trow) * ldc + n0;
+    const bool row_in = m0 + trow < M;
+    float* crow = C + (long long)(row_in ? m0 + trow : 0) * ldc + n0;
+    // columns [n0, n0 + ncols) exist; whole 16-byte groups when N % 4 == 0
+    const int ncols = N - n0 < BN ? N - n0 : BN;
+    auto store4 = [&](int col, float4 v) {  // col: tile column of v.x
+      if (!row_in) return;
+      if (N % 4 == 0 && col + 4 <= ncols) {
+        *reinterpret_cast<float4*>(crow + col) = v;
+      } else {
+        if (col < ncols) crow[col] = v.x;
+        if (col + 1 < ncols) crow[col + 1] = v.y;
+        if (col + 2 < ncols) crow[col + 2] = v.z;
+        if (col + 3 < ncols) crow[col + 3] = v.w;
+      }
+    };
     // split tiles: this CTA's half of the parked second-K-half tile and its flag
     float* wrow = ws + ((long long)(unit >> 1) * 256 + trow) * BN;
     unsigned* flag = flags + 2 * (unit >> 1) + rank;
@@ -499,9 +516,8 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
       if (!split) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
-          *reinterpret_cast<float4*>(crow + c0 + j) =
-              make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                          __uint_as_float(r[j + 3]));
+          store4(c0 + j, make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                                     __uint_as_float(r[j + 3])));
         }
       } else if (khalf == 1) {
 #pragma unroll
@@ -514,9 +530,9 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
           const float4 w = __ldcg(reinterpret_cast<const float4*>(wrow + c0 + j));
-          *reinterpret_cast<float4*>(crow + c0 + j) =
-              make_float4(__fadd_rn(__uint_as_float(r[j]), w.x), __fadd_rn(__uint_as_float(r[j + 1]), w.y),
-                          __fadd_rn(__uint_as_float(r[j + 2]), w.z), __fadd_rn(__uint_as_float(r[j + 3]), w.w));
+          store4(c0 + j,
+                 make_float4(__fadd_rn(__uint_as_float(r[j]), w.x), __fadd_rn(__uint_as_float(r[j + 1]), w.y),
+                             __fadd_rn(__uint_as_float(r[j + 2]), w.z), __fadd_rn(__uint_as_float(r[j + 3]), w.w)));
         }
       }
     }

@@ -105,8 +105,10 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
             "b_major": "mn" if b_mn else "k",
             "fmad": False,
             "order": "3xtf32 tensor-core, CTA pairs; tail tiles K-split in two halves (reassociated)",
-            "pre": [f"({py_expr(M)}) % 256 == 0", f"({py_expr(N)}) % {PAIR_BN} == 0", f"({py_expr(K)}) % 32 == 0",
-                    f"({py_expr(M)}) * ({py_expr(N)}) * ({py_expr(K)}) > 0"],
+            # ragged M / N / K: TMA zero-fill + a guarded epilogue; the 16-byte
+            # row pitch of the TMA views needs K % 4 (and N % 4 for MN-major B)
+            "pre": [f"({py_expr(K)}) % 4 == 0", f"({py_expr(M)}) * ({py_expr(N)}) * ({py_expr(K)}) > 0"]
+                   + ([f"({py_expr(N)}) % 4 == 0"] if b_mn else []),
             "smem": PAIR_STAGES * 2 * (128 * 32 * 4 + (PAIR_BN // 2) * 32 * 4) + 1024 + 256,
             "extra_args": [
                 {"kind": "tma2d", "buf": a_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(M)],
@@ -153,16 +155,20 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
 SPLIT_SLOTS_MAX = 74  # workspace sizing: at most this many split tiles (one wave of B200 SM pairs)
 
 
+def pair_tiles(M, N, bn):
+    return -(-M // 256) * -(-N // bn)
+
+
 def full_tiles(M, N, K, bn, sm):
     """How many 256 x bn pair tiles run whole.  The tail past the last whole
     wave of SM pairs is split along K into two units per tile when those
     units fit in one wave (else nothing is split).  RISE_GEMM_KSPLIT=0
     disables the split."""
-    tiles = (M // 256) * (N // bn)
+    tiles = pair_tiles(M, N, bn)
     slots = max(1, sm // 2)
     tail = tiles % slots
     if (os.environ.get("RISE_GEMM_KSPLIT", "1") != "1" or tail == 0 or tiles < slots or 2 * tail > slots
-            or tail > SPLIT_SLOTS_MAX or K // 32 < 2):
+            or tail > SPLIT_SLOTS_MAX or -(-K // 32) < 2):
         return tiles
     return tiles - tail
 
@@ -174,7 +180,7 @@ def launch(st, nats, sm):
     N = eval_py(st["N"], nats)
     if st.get("pair"):
         K = eval_py(st["K"], nats)
-        tiles = (M // 256) * (N // st["bn"])
+        tiles = pair_tiles(M, N, st["bn"])
         nfull = full_tiles(M, N, K, st["bn"], sm)
         pairs = nfull + 2 * (tiles - nfull)
         return (2 * pairs, 1, 1), (192, 1, 1), st["smem"], (2, 1, 1)

@@ -254,13 +254,33 @@ def test_sgemm_generic_exact_bit_exact(gpu):
     np.testing.assert_array_equal(got, oracle.sgemm_bt(A, Bt))
 
 
-def test_sgemm_falls_back_when_tiles_do_not_divide(gpu):
-    c = compile_program(programs.SGEMM_BT, None, name="sgemm")
+@pytest.mark.parametrize("n,m,k", [(100, 36, 24), (300, 200, 100), (257, 513, 36), (1, 7, 4), (4100, 4096, 4100)])
+@pytest.mark.parametrize("natural", [False, True])
+def test_sgemm_ragged_shapes_on_the_tensor_cores(gpu, n, m, k, natural):
+    """Shapes that do not divide the 256 x 256 x 32 tiles: the TMA unit
+    zero-fills the edge tiles and the epilogue stores only in-range cells
+    (B row-major needs m % 4 == 0 for its 16-byte TMA pitch, else the
+    generic kernel runs, bit-exact)."""
+    from paper_2201_03611_b200.run import Executable
+
+    src = programs.SGEMM if natural else programs.SGEMM_BT
+    c = compile_program(src, None, name="sgemm")
     code = emit_cuda(c.unit)
-    A = oracle.rng_inputs(4, 100, 24)
-    Bt = oracle.rng_inputs(5, 36, 24)
-    got = run_cuda(code, c.unit, {"n": 100, "m": 36, "k": 24}, [A, Bt], as_numpy=True).reshape(100, 36)
-    np.testing.assert_array_equal(got, oracle.sgemm_bt(A, Bt))
+    A = oracle.rng_inputs(4, n, k)
+    Bt = oracle.rng_inputs(5, m, k)
+    B_in = np.ascontiguousarray(Bt.T) if natural else Bt
+    nats = {"n": n, "m": m, "k": k}
+    got = run_cuda(code, c.unit, nats, [A, B_in], as_numpy=True).reshape(n, m)
+    kinds = Executable(code, nats).template_kinds
+    if natural and m % 4:
+        assert kinds == ["grid"]
+        np.testing.assert_array_equal(got, oracle.sgemm_bt(A, Bt))
+        return
+    assert kinds == ["gemm_tc"]
+    rows = slice(max(0, n - 300), n)
+    C64, absC = oracle.sgemm_bt_f64(A[rows], Bt)
+    err = np.abs(got[rows] - C64)
+    assert np.all(err <= oracle.gemm_bound(k, absC)), float(np.max(err / (absC * oracle.U * k)))
 
 
 def test_tensor_core_ignores_low_tf32_bits(gpu):

@@ -229,12 +229,13 @@ REDUCE_EARLY = os.environ.get("RISE_REDUCE_EARLY", "1") == "1"  # 2-D tensor-map
 def reduce_fold_length(n: int) -> int:
     """Terms one thread folds sequentially in phase 1 of the `reduce`
     template for n terms (its error bound's sequential part)."""
-    n4 = -(-n // 4)
+    n4 = n // 4
+    tail = n - 4 * n4  # folded after the float4 part by the last block
     if REDUCE_TMA:
         ch4 = REDUCE_TMA_CHUNK // 16
         chunks = -(-n4 // ch4)
-        return 4 * -(-chunks // REDUCE_TMA_GRID) * -(-ch4 // REDUCE_BLOCK)
-    return 4 * -(-n4 // (REDUCE_GRID * REDUCE_BLOCK))
+        return 4 * -(-chunks // REDUCE_TMA_GRID) * -(-ch4 // REDUCE_BLOCK) + tail
+    return 4 * -(-n4 // (REDUCE_GRID * REDUCE_BLOCK)) + tail
 
 
 def _match_reduce(prog, stage, base_name, temps, exact):
@@ -272,7 +273,7 @@ def _match_reduce(prog, stage, base_name, temps, exact):
         for t in lir.walk(s):
             if isinstance(t, lir.Assign) and isinstance(t.target, lir.ScalarRef) and t.target != acc:
                 return None
-    pre = [f"({py_expr(loop.bound)}) % 4 == 0"]
+    pre = []  # any n: the n % 4 tail is folded by the last block (below)
     for _b, base in streams.values():
         pre.append(f"({py_expr(base)}) % 4 == 0")
     pre = list(dict.fromkeys(pre))
@@ -294,6 +295,13 @@ def _match_reduce(prog, stage, base_name, temps, exact):
 
         return ValueRenderer(prog, exact, load_hook=hook)(term)
 
+    def tail_hook(ld):
+        if ld in streams:
+            buf, base = streams[ld]
+            return f"{buf}[({r(base)}) + rs_j]"
+        return None
+
+    tail_term = ValueRenderer(prog, exact, load_hook=tail_hook)(term)
     shfl = "__shfl_xor_sync(0xffffffffu, rs_s, rs_o)"
     U = REDUCE_BATCH
     tma = REDUCE_TMA
@@ -464,6 +472,8 @@ def _match_reduce(prog, stage, base_name, temps, exact):
         "#pragma unroll",
         f"    for (int rs_o = 16; rs_o > 0; rs_o >>= 1) rs_s = {add('rs_s', shfl)};",
         "    if (threadIdx.x == 0) {",
+        "      // the n % 4 tail terms, in order, after the folded float4 part",
+        f"      for (int rs_j = 4 * RS_N4; rs_j < {r(loop.bound)}; ++rs_j) rs_s = {add('rs_s', tail_term)};",
         f"      {ct} {acc.name} = {vr_plain(init.value)};",
         f"      {acc.name} = {add(acc.name, 'rs_s')};",
     ]

@@ -20,19 +20,21 @@ def _cfg(key):
     return compile_program(cfg["source"], cfg["strategy"], name=cfg["name"])
 
 
-@pytest.mark.parametrize("n", [0, 4, 5, 7, 12])
-def test_dot_small_and_empty(gpu, n):
+@pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 7, 12, 1000003])
+def test_dot_small_empty_and_ragged(gpu, n):
     c = _cfg("dot")
     a = oracle.rng_inputs(1, n)
     b = oracle.rng_inputs(2, n)
     got = run_cuda(emit_cuda(c.unit), c.unit, {"n": n}, [a, b], as_numpy=True)[0]
-    if n % 4:  # generic sequential kernel: the reference's own order
-        assert got == oracle.dot(a, b)
-    else:
-        v64, s = oracle.dot_f64(a, b)
-        assert abs(float(got) - v64) <= oracle.reassociated_dot_bound(max(n, 1), s, 4) + 0.0
+    from paper_2201_03611_b200 import idioms
+
+    # the reduce template for any n (the n % 4 tail folded last)
+    v64, s = oracle.dot_f64(a, b)
+    assert abs(float(got) - v64) <= oracle.reassociated_dot_bound(max(n, 1), s, idioms.reduce_fold_length(n))
     if n == 0:
         assert got == np.float32(0.0)
+    if n < 4:  # only tail terms: the reference's own left fold
+        assert got == oracle.dot(a, b)
 
 
 @pytest.mark.parametrize("n,m", [(1, 4), (3, 5), (1, 1), (31, 6), (64, 1028)])

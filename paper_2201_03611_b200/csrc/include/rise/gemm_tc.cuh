@@ -557,4 +557,240 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
   }
 }
 
+// Persistent form of gemm_3xtf32_2sm: one CTA pair per SM pair, looping over
+// the same work units (whole tiles, then the K-split tail units) — unit u
+// goes to pair u % P, so each pair owns at most one split unit, its last.
+// The accumulator is double-buffered in TMEM (2 x BN columns): the MMA
+// issuer fills slot i & 1 while four dedicated epilogue warps drain the
+// other, so a tile's epilogue and the next tile's prologue overlap its
+// neighbour's main loop.  Barriers: the stage ring (full / conv / empty) runs
+// on a counter global to the pair's units; tmem_full[2] (MMA commit,
+// multicast to both CTAs) and tmem_empty[2] (in CTA 0, one arrival per
+// CTA's epilogue).  Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer,
+// 2..5 hi/lo converters, 6..9 epilogue (TMEM lane quarter = warp % 4).
+constexpr int PTHREADS = 320;
+
+template <int M, int N, int K, int BN, int STAGES, bool B_MN = false>
+RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const rs_tmap* mapA, const rs_tmap* mapB,
+                                          int n_full, int n_units, float* __restrict__ ws,
+                                          unsigned* __restrict__ flags) {
+  using G = Cfg2<BN, STAGES>;
+  extern __shared__ __align__(1024) unsigned char rs_gemm_smem_raw[];
+  unsigned char* smem =
+      rs_gemm_smem_raw + ((1024u - (rs_smem_addr(rs_gemm_smem_raw) & 1023u)) & 1023u);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + STAGES * G::STAGE_BYTES);
+  unsigned long long* full = bars;
+  unsigned long long* conv = bars + STAGES;
+  unsigned long long* empty = bars + 2 * STAGES;
+  unsigned long long* tmem_full = bars + 3 * STAGES;       // [2]
+  unsigned long long* tmem_empty = bars + 3 * STAGES + 2;  // [2]
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 3 * STAGES + 4);
+  unsigned char* sig_slot = reinterpret_cast<unsigned char*>(bars) + ((3 * STAGES + 5) * 8 + 15) / 16 * 16;
+
+  constexpr int KB = (K + BK - 1) / BK;
+  constexpr int NTN = (N + BN - 1) / BN;
+  const unsigned rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto a_raw = [&](int s) { return smem + s * G::STAGE_BYTES; };
+  auto a_lo = [&](int s) { return smem + s * G::STAGE_BYTES + G::TILE_A; };
+  auto b_raw = [&](int s) { return smem + s * G::STAGE_BYTES + 2 * G::TILE_A; };
+  auto b_lo = [&](int s) { return smem + s * G::STAGE_BYTES + 2 * G::TILE_A + G::TILE_B; };
+  // unit -> (tile, K range, split half)
+  auto unit_of = [&](int u, int& m0, int& n0, int& kb0, int& kb1, int& khalf, int& sidx) {
+    const bool split = u >= n_full;
+    sidx = split ? u - n_full : -1;
+    const int tile = split ? n_full + (sidx >> 1) : u;
+    khalf = split ? (sidx & 1) : 0;
+    kb0 = split && khalf ? KB / 2 : 0;
+    kb1 = split && !khalf ? KB / 2 : KB;
+    m0 = (tile / NTN) * 256;
+    n0 = (tile % NTN) * BN;
+  };
+
+  if (threadIdx.x == 0) {
+    rs_tmap_prefetch(mapA);
+    rs_tmap_prefetch(mapB);
+    for (int s = 0; s < STAGES; ++s) {
+      rs_mbar_init(&full[s], 1);
+      rs_mbar_init(&conv[s], 1);
+      rs_mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      rs_mbar_init(&tmem_full[a], 1);
+      rs_mbar_init(&tmem_empty[a], 2);  // one arrival from each CTA's epilogue (CTA 0's copy is used)
+    }
+    rs_fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc2<2 * G::TMEM_COLS>(tmem_slot);
+  fence_before();
+  cluster_sync();
+  fence_after();
+  const unsigned tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0;
+      for (int u = pair; u < n_units; u += npairs) {
+        int m0, n0, kb0, kb1, khalf, sidx;
+        unit_of(u, m0, n0, kb0, kb1, khalf, sidx);
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
+          const int s = g % STAGES;
+          const unsigned ph = (unsigned)((g / STAGES) & 1);
+          rs_mbar_wait(&empty[s], ph ^ 1u);
+          rs_mbar_arrive_expect_tx(&full[s], G::TILE_A + G::TILE_B);
+          rs_tma_load_2d(a_raw(s), mapA, kb * BK, m0 + 128 * (int)rank, &full[s]);
+          if (B_MN) {
+#pragma unroll
+            for (int b = 0; b < BN / 64; ++b)
+              rs_tma_load_2d(b_raw(s) + b * 4096, mapB, n0 + (BN / 2) * (int)rank + 32 * b, kb * BK, &full[s]);
+          } else {
+            rs_tma_load_2d(b_raw(s), mapB, kb * BK, n0 + (BN / 2) * (int)rank, &full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      int g = 0, i = 0;
+      constexpr unsigned idesc = B_MN ? G::IDESC_BMN : G::IDESC;
+      for (int u = pair; u < n_units; u += npairs, ++i) {
+        int m0, n0, kb0, kb1, khalf, sidx;
+        unit_of(u, m0, n0, kb0, kb1, khalf, sidx);
+        const int slot = i & 1;
+        if (i >= 2) mbar_wait_cluster(&tmem_empty[slot], (unsigned)(((i >> 1) & 1) ^ 1));
+        fence_after();
+        const unsigned acc = tmem + (unsigned)(slot * BN);
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
+          const int s = g % STAGES;
+          const unsigned ph = (unsigned)((g / STAGES) & 1);
+          mbar_wait_cluster(&conv[s], ph);
+          fence_after();
+          const unsigned long long ahi = smem_desc(rs_smem_addr(a_raw(s)));
+          const unsigned long long alo = smem_desc(rs_smem_addr(a_lo(s)));
+          const unsigned long long bhi =
+              B_MN ? smem_desc_mn(rs_smem_addr(b_raw(s))) : smem_desc(rs_smem_addr(b_raw(s)));
+          const unsigned long long blo =
+              B_MN ? smem_desc_mn(rs_smem_addr(b_lo(s))) : smem_desc(rs_smem_addr(b_lo(s)));
+#pragma unroll
+          for (int k = 0; k < BK / 8; ++k) {
+            const unsigned long long off = (unsigned long long)(k * 32) >> 4;
+            const unsigned long long boff = B_MN ? (unsigned long long)(k * 1024) >> 4 : off;
+            mma2(acc, alo + off, bhi + boff, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            mma2(acc, ahi + off, blo + boff, idesc, 1u);
+            mma2(acc, ahi + off, bhi + boff, idesc, 1u);
+          }
+          commit2_multicast(&empty[s]);
+        }
+        commit2_multicast(&tmem_full[slot]);
+      }
+    }
+    __syncwarp();
+  } else if (warp < 6) {
+    const int t = threadIdx.x - 64;
+    int g = 0;
+    for (int u = pair; u < n_units; u += npairs) {
+      int m0, n0, kb0, kb1, khalf, sidx;
+      unit_of(u, m0, n0, kb0, kb1, khalf, sidx);
+      for (int kb = kb0; kb < kb1; ++kb, ++g) {
+        const int s = g % STAGES;
+        const unsigned ph = (unsigned)((g / STAGES) & 1);
+        rs_mbar_wait(&full[s], ph);
+        split_tile<false>(a_raw(s), a_lo(s), G::TILE_A, t);
+        split_tile<false>(b_raw(s), b_lo(s), G::TILE_B, t);
+        rs_fence_proxy_async();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (t == 0) {
+          if (rank == 0) {
+            rs_mbar_arrive_expect_tx(&conv[s], 16u);
+          } else {
+            signal_s2s_cluster(mapa(rs_smem_addr(sig_slot), 0u), sig_slot, mapa(rs_smem_addr(&conv[s]), 0u));
+          }
+        }
+      }
+    }
+  } else {
+    // epilogue warps 6..9
+    const int t = threadIdx.x - 192;
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int trow = 128 * (int)rank + row;
+    int i = 0;
+    for (int u = pair; u < n_units; u += npairs, ++i) {
+      int m0, n0, kb0, kb1, khalf, sidx;
+      unit_of(u, m0, n0, kb0, kb1, khalf, sidx);
+      const bool split = sidx >= 0;
+      const int slot = i & 1;
+      rs_mbar_wait(&tmem_full[slot], (unsigned)((i >> 1) & 1));
+      fence_after();
+      const bool row_in = m0 + trow < M;
+      float* crow = C + (long long)(row_in ? m0 + trow : 0) * ldc + n0;
+      const int ncols = N - n0 < BN ? N - n0 : BN;
+      auto store4 = [&](int col, float4 v) {
+        if (!row_in) return;
+        if (N % 4 == 0 && col + 4 <= ncols) {
+          *reinterpret_cast<float4*>(crow + col) = v;
+        } else {
+          if (col < ncols) crow[col] = v.x;
+          if (col + 1 < ncols) crow[col + 1] = v.y;
+          if (col + 2 < ncols) crow[col + 2] = v.z;
+          if (col + 3 < ncols) crow[col + 3] = v.w;
+        }
+      };
+      float* wrow = ws + ((long long)(split ? sidx >> 1 : 0) * 256 + trow) * BN;
+      unsigned* flag = flags + 2 * (split ? sidx >> 1 : 0) + rank;
+      if (split && khalf == 0) {
+        unsigned v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        } while (v == 0u);
+      }
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        unsigned r[32];
+        tmem_ld32(tmem + (unsigned)(slot * BN) + ((unsigned)(q * 32) << 16) + (unsigned)c0, r);
+        if (!split) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            store4(c0 + j, make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                                       __uint_as_float(r[j + 3])));
+        } else if (khalf == 1) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            __stcg(reinterpret_cast<float4*>(wrow + c0 + j),
+                   make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                               __uint_as_float(r[j + 3])));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 w = __ldcg(reinterpret_cast<const float4*>(wrow + c0 + j));
+            store4(c0 + j, make_float4(__fadd_rn(__uint_as_float(r[j]), w.x), __fadd_rn(__uint_as_float(r[j + 1]), w.y),
+                                       __fadd_rn(__uint_as_float(r[j + 2]), w.z),
+                                       __fadd_rn(__uint_as_float(r[j + 3]), w.w)));
+          }
+        }
+      }
+      // this CTA's share of the slot is drained (and the parked tile used)
+      fence_before();
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (t == 0) {
+        if (split && khalf == 1) {
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(1u) : "memory");
+        } else if (split) {
+          *flag = 0u;
+        }
+        if (rank == 0) rs_mbar_arrive(&tmem_empty[slot]);
+        else mbar_arrive_remote(mapa(rs_smem_addr(&tmem_empty[slot]), 0u));
+      }
+    }
+  }
+  fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    fence_after();
+    tmem_dealloc2<2 * G::TMEM_COLS>(tmem);
+  }
+}
+
 }  // namespace rise_gemm

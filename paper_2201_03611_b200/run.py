@@ -202,6 +202,12 @@ class Executable:
             if table is None:
                 raise InterpreterError("peer-source kernel launched without buffers['rs_peer_table']")
             return ctypes.c_void_p(_dptr(table))
+        if kind == "gemm_units":
+            from .tmpl_gemm import full_tiles, pair_tiles
+
+            M, N, K = (eval_py(extra[k], self.nats) for k in ("M", "N", "K"))
+            nfull = full_tiles(M, N, K, extra["bn"], self.sm_count)
+            return ctypes.c_int(nfull + 2 * (pair_tiles(M, N, extra["bn"]) - nfull))
         if kind == "gemm_full_tiles":
             from .tmpl_gemm import full_tiles
 

@@ -32,6 +32,9 @@ WRITE_HI = os.environ.get("RISE_GEMM_WRITE_HI", "0") == "1"
 PAIR = os.environ.get("RISE_GEMM_2SM", "1") == "1"
 PAIR_BN = int(os.environ.get("RISE_GEMM_PAIR_BN", "256"))
 PAIR_STAGES = int(os.environ.get("RISE_GEMM_PAIR_STAGES", "3"))
+# persistent CTA pairs with a double-buffered TMEM accumulator and dedicated
+# epilogue warps (gemm_3xtf32_2sm_persistent)
+PERSIST = os.environ.get("RISE_GEMM_PERSIST", "1") == "1"  # measured 278 -> 284 TFLOP/s
 
 
 def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
@@ -86,12 +89,17 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
     extra = ["const __grid_constant__ rs_tmap rs_mapA", "const __grid_constant__ rs_tmap rs_mapB"]
     if PAIR:
         extra += ["int rs_nfull", "float* __restrict__ rs_ws", "unsigned* __restrict__ rs_flags"]
-    lines = kernel_head(prog, name, temps, launch_bounds="192, 1", extra_params=extra)
+        if PERSIST:
+            extra.insert(3, "int rs_nunits")
+    threads = 320 if (PAIR and PERSIST) else 192
+    lines = kernel_head(prog, name, temps, launch_bounds=f"{threads}, 1", extra_params=extra)
     if PAIR:
+        fn = "gemm_3xtf32_2sm_persistent" if PERSIST else "gemm_3xtf32_2sm"
+        args = "rs_nfull, rs_nunits, rs_ws, rs_flags" if PERSIST else "rs_nfull, rs_ws, rs_flags"
         lines += [
-            f"  rise_gemm::gemm_3xtf32_2sm<{r(M)}, {r(N)}, {r(K)}, {PAIR_BN}, {PAIR_STAGES}, "
+            f"  rise_gemm::{fn}<{r(M)}, {r(N)}, {r(K)}, {PAIR_BN}, {PAIR_STAGES}, "
             f"{'true' if b_mn else 'false'}>"
-            f"({st.target.buf}, {r(N)}, &rs_mapA, &rs_mapB, rs_nfull, rs_ws, rs_flags);",
+            f"({st.target.buf}, {r(N)}, &rs_mapA, &rs_mapB, {args});",
             "}",
         ]
         plan = {
@@ -103,6 +111,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
             "bn": PAIR_BN,
             "pair": True,
             "b_major": "mn" if b_mn else "k",
+            "persistent": PERSIST,
             "fmad": False,
             "order": "3xtf32 tensor-core, CTA pairs; tail tiles K-split in two halves (reassociated)",
             # ragged M / N / K: TMA zero-fill + a guarded epilogue; the 16-byte
@@ -118,6 +127,8 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
                  {"kind": "tma2d", "buf": b_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(N)],
                   "pitch": py_expr(K), "box": [32, PAIR_BN // 2], "swizzle": 3}),
                 {"kind": "gemm_full_tiles", "M": py_expr(M), "N": py_expr(N), "K": py_expr(K), "bn": PAIR_BN},
+                *([{"kind": "gemm_units", "M": py_expr(M), "N": py_expr(N), "K": py_expr(K), "bn": PAIR_BN}]
+                  if PERSIST else []),
                 {"kind": "workspace", "name": f"rs_ws_{base_name}_ktail"},
                 {"kind": "workspace", "name": f"rs_ws_{base_name}_kflags"},
             ],
@@ -182,6 +193,8 @@ def launch(st, nats, sm):
         K = eval_py(st["K"], nats)
         tiles = pair_tiles(M, N, st["bn"])
         nfull = full_tiles(M, N, K, st["bn"], sm)
-        pairs = nfull + 2 * (tiles - nfull)
-        return (2 * pairs, 1, 1), (192, 1, 1), st["smem"], (2, 1, 1)
+        units = nfull + 2 * (tiles - nfull)
+        if st.get("persistent"):  # one pair per SM pair, looping over the units
+            return (2 * max(1, min(units, sm // 2)), 1, 1), (320, 1, 1), st["smem"], (2, 1, 1)
+        return (2 * units, 1, 1), (192, 1, 1), st["smem"], (2, 1, 1)
     return (N // st["bn"], M // 128, 1), (192, 1, 1), st["smem"], (1, 1, 1)

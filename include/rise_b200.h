@@ -125,6 +125,15 @@ int rs_event_record(void* event, void* stream);
 int rs_event_synchronize(void* event);
 int rs_event_elapsed_ms(float* ms, void* start, void* end);
 
+/* ---- CUDA graphs (launch-bound multi-kernel steps) --------------------
+ * Capture everything enqueued on `stream` between begin and end (e.g. every
+ * stage of a multi-kernel unit, bound once) into an executable graph, then
+ * replay it with one launch.  Replaces: nothing (cexec interprets text). */
+int rs_graph_capture_begin(void* stream);
+int rs_graph_capture_end(void* stream, void** graph_exec);
+int rs_graph_launch(void* graph_exec, void* stream);
+int rs_graph_destroy(void* graph_exec);
+
 /* ---- TMA ------------------------------------------------------------- */
 
 /* Encode a 2-D (inner dim0, outer dim1) tiled TMA descriptor for fp32 data

@@ -74,6 +74,12 @@ struct Driver {
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
   CUresult (*GetErrorString)(CUresult, const char**);
+  CUresult (*StreamBeginCapture)(CUstream, CUstreamCaptureMode);
+  CUresult (*StreamEndCapture)(CUstream, CUgraph*);
+  CUresult (*GraphInstantiate)(CUgraphExec*, CUgraph, unsigned long long);
+  CUresult (*GraphLaunch)(CUgraphExec, CUstream);
+  CUresult (*GraphExecDestroy)(CUgraphExec);
+  CUresult (*GraphDestroy)(CUgraph);
   CUresult (*IpcGetMemHandle)(CUipcMemHandle*, CUdeviceptr);
   CUresult (*IpcOpenMemHandle)(CUdeviceptr*, CUipcMemHandle, unsigned);
   CUresult (*IpcCloseMemHandle)(CUdeviceptr);
@@ -127,6 +133,12 @@ int load_driver() {
   ok &= sym(g_drv.EventElapsedTime, "cuEventElapsedTime");
   ok &= sym(g_drv.TensorMapEncodeTiled, "cuTensorMapEncodeTiled");
   ok &= sym(g_drv.GetErrorString, "cuGetErrorString");
+  ok &= sym(g_drv.StreamBeginCapture, "cuStreamBeginCapture_v2");
+  ok &= sym(g_drv.StreamEndCapture, "cuStreamEndCapture");
+  ok &= sym(g_drv.GraphInstantiate, "cuGraphInstantiateWithFlags");
+  ok &= sym(g_drv.GraphLaunch, "cuGraphLaunch");
+  ok &= sym(g_drv.GraphExecDestroy, "cuGraphExecDestroy");
+  ok &= sym(g_drv.GraphDestroy, "cuGraphDestroy");
   ok &= sym(g_drv.IpcGetMemHandle, "cuIpcGetMemHandle");
   ok &= sym(g_drv.IpcOpenMemHandle, "cuIpcOpenMemHandle_v2");
   ok &= sym(g_drv.IpcCloseMemHandle, "cuIpcCloseMemHandle");
@@ -516,6 +528,38 @@ int rs_event_synchronize(void* event) {
 int rs_event_elapsed_ms(float* ms, void* start, void* end) {
   if (int e = ensure_ctx()) return e;
   CU(g_drv.EventElapsedTime(ms, (CUevent)start, (CUevent)end), "cuEventElapsedTime");
+  return 0;
+}
+
+int rs_graph_capture_begin(void* stream) {
+  if (int e = ensure_ctx()) return e;
+  if (!stream) return fail("rs_graph_capture_begin: capture needs a non-default stream");
+  CU(g_drv.StreamBeginCapture((CUstream)stream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL), "cuStreamBeginCapture");
+  return 0;
+}
+
+int rs_graph_capture_end(void* stream, void** graph_exec) {
+  if (int e = ensure_ctx()) return e;
+  CUgraph g = nullptr;
+  CU(g_drv.StreamEndCapture((CUstream)stream, &g), "cuStreamEndCapture");
+  CUgraphExec x = nullptr;
+  CUresult r = g_drv.GraphInstantiate(&x, g, 0);
+  g_drv.GraphDestroy(g);
+  CU(r, "cuGraphInstantiate");
+  *graph_exec = (void*)x;
+  return 0;
+}
+
+int rs_graph_launch(void* graph_exec, void* stream) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.GraphLaunch((CUgraphExec)graph_exec, (CUstream)stream), "cuGraphLaunch");
+  return 0;
+}
+
+int rs_graph_destroy(void* graph_exec) {
+  if (!graph_exec) return 0;
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.GraphExecDestroy((CUgraphExec)graph_exec), "cuGraphExecDestroy");
   return 0;
 }
 

@@ -183,6 +183,14 @@ class Executable:
         launch_all.prepared = prepared
         return launch_all
 
+    def graph(self, buffers: dict, stream):
+        """bind() captured into a CUDA graph: one launch replays every stage
+        of the unit (`stream` must be a non-default stream)."""
+        launch_all = self.bind(buffers, stream)
+        g = rt.Graph(launch_all, stream)
+        g.prepared = launch_all.prepared  # keep the argument arrays alive
+        return g
+
     def _extra_arg(self, extra, buffers, temps):
         kind = extra["kind"]
         if kind == "workspace":

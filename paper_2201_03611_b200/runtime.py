@@ -35,6 +35,7 @@ EXPORTED = (
     "rs_event_destroy", "rs_event_record", "rs_event_synchronize", "rs_event_elapsed_ms",
     "rs_tma_desc_2d_f32", "rs_ipc_handle", "rs_ipc_open", "rs_ipc_close", "rs_halo_exchange",
     "rs_comm_unique_id", "rs_comm_init", "rs_comm_destroy", "rs_allgather",
+    "rs_graph_capture_begin", "rs_graph_capture_end", "rs_graph_launch", "rs_graph_destroy",
 )
 
 _lib = None
@@ -98,6 +99,10 @@ def lib():
             L.rs_comm_init.argtypes = [ctypes.POINTER(vp), i, i, vp]
             L.rs_comm_destroy.argtypes = [vp]
             L.rs_allgather.argtypes = [vp, vp, vp, sz, vp]
+            L.rs_graph_capture_begin.argtypes = [vp]
+            L.rs_graph_capture_end.argtypes = [vp, ctypes.POINTER(vp)]
+            L.rs_graph_launch.argtypes = [vp, vp]
+            L.rs_graph_destroy.argtypes = [vp]
             _lib = L
     return _lib
 
@@ -420,3 +425,32 @@ class NcclComm:
         if self.h:
             check_run(lib().rs_comm_destroy(self.h), "rs_comm_destroy")
             self.h = ctypes.c_void_p()
+
+
+# CUDA graphs ------------------------------------------------------------------
+
+
+class Graph:
+    """Everything `record()` enqueues on `stream` (a torch CUDA stream or a
+    raw CUstream), captured once into an executable graph; `__call__`
+    replays it with a single launch on that stream."""
+
+    def __init__(self, record, stream):
+        init()
+        self.stream = _stream_ptr(stream)
+        self.h = ctypes.c_void_p()
+        check_run(lib().rs_graph_capture_begin(self.stream), "rs_graph_capture_begin")
+        try:
+            record()
+        finally:
+            check_run(lib().rs_graph_capture_end(self.stream, ctypes.byref(self.h)), "rs_graph_capture_end")
+
+    def __call__(self):
+        check_run(lib().rs_graph_launch(self.h, self.stream), "rs_graph_launch")
+
+    def __del__(self):
+        try:
+            if self.h and _lib is not None:
+                _lib.rs_graph_destroy(self.h)
+        except Exception:  # noqa: BLE001
+            pass

@@ -119,3 +119,30 @@ def test_stream_host_pipelines_every_step(gpu):
     assert ms > 0
     for o, w in zip(outs, want):
         np.testing.assert_array_equal(o.numpy(), w)
+
+
+def test_cuda_graph_replays_a_multi_kernel_unit(gpu):
+    """Executable.graph: every stage of a unit (here the chunked dot's
+    rowfold + seqfold) captured once into a CUDA graph and replayed; each
+    replay gives the bit-identical result of the direct launch."""
+    import torch
+
+    from paper_2201_03611_b200 import gpu_rules
+    from paper_2201_03611_b200.run import Executable
+
+    c = compile_program(programs.DOT, gpu_rules.CHUNKED_REDUCE_STRATEGY, name="dotChunked")
+    n = 1 << 20
+    exe = Executable(emit_cuda(c.unit, reassociate=False), {"n": n})
+    assert len(exe.kernels) == 2
+    a = torch.from_numpy(oracle.rng_inputs(1, n)).cuda()
+    b = torch.from_numpy(oracle.rng_inputs(11, n)).cuda()
+    want = exe(a, b).cpu().numpy()
+    out = torch.zeros(1, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.Stream()
+    g = exe.graph({"a": a, "b": b, "output": out}, stream)
+    for _ in range(3):
+        out.zero_()
+        torch.cuda.synchronize()
+        g()
+        stream.synchronize()
+        np.testing.assert_array_equal(out.cpu().numpy(), want)

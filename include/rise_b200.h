@@ -104,6 +104,15 @@ int rs_function_attribute(rs_function f, int attribute, int* value);
 int rs_launch(rs_function f, const unsigned grid[3], const unsigned block[3],
               const unsigned cluster[3], unsigned smem, void* stream, void** args);
 
+/* rs_launch with launch flags: RS_LAUNCH_COOPERATIVE (all blocks co-resident,
+ * for kernels with grid-wide barriers; the launch fails rather than hangs
+ * when the grid does not fit) and RS_LAUNCH_PDL (programmatic dependent
+ * launch: may start while the previous kernel in the stream drains). */
+#define RS_LAUNCH_COOPERATIVE 1u
+#define RS_LAUNCH_PDL 2u
+int rs_launch_ex(rs_function f, const unsigned grid[3], const unsigned block[3],
+                 const unsigned cluster[3], unsigned smem, void* stream, void** args, unsigned flags);
+
 /* ---- memory (replaces cexec.flatten_value/unflatten_value, cexec.py:533-552) */
 
 int rs_malloc(void** dptr, size_t bytes);

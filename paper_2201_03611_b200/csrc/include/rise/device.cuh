@@ -146,5 +146,26 @@ RS_DEVICE float4 rs_ldg_stream(const float4* p) {
   return r;
 }
 
+// Grid-wide barrier for kernels launched cooperatively (RS_LAUNCH_COOPERATIVE:
+// every block co-resident).  bar[0] counts arrivals, bar[1] is the
+// generation; both start at 0 (a zeroed workspace) and bar[0] returns to 0.
+RS_DEVICE void rs_grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;  // read before arriving: the last arrival may bump it
+    __threadfence();          // this block's writes before its arrival
+    if (atomicAdd(bar, 1u) == gridDim.x * gridDim.y * gridDim.z - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(64);
+    }
+    __threadfence();  // everyone's writes before this block continues
+  }
+  __syncthreads();
+}
+
 RS_DEVICE unsigned rs_lane() { return threadIdx.x & 31u; }
 RS_DEVICE unsigned rs_warp() { return threadIdx.x >> 5; }

@@ -406,6 +406,11 @@ int rs_function_attribute(rs_function f, int attribute, int* value) {
 
 int rs_launch(rs_function f, const unsigned grid[3], const unsigned block[3], const unsigned cluster[3],
               unsigned smem, void* stream, void** args) {
+  return rs_launch_ex(f, grid, block, cluster, smem, stream, args, 0u);
+}
+
+int rs_launch_ex(rs_function f, const unsigned grid[3], const unsigned block[3], const unsigned cluster[3],
+                 unsigned smem, void* stream, void** args, unsigned flags) {
   if (int e = ensure_ctx()) return e;
   if (smem > 48 * 1024 && (int)smem > f->smem_optin) {
     CU(g_drv.FuncSetAttribute(f->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem),
@@ -422,14 +427,28 @@ int rs_launch(rs_function f, const unsigned grid[3], const unsigned block[3], co
   cfg.blockDimZ = block[2];
   cfg.sharedMemBytes = smem;
   cfg.hStream = (CUstream)stream;
-  CUlaunchAttribute attr[1];
+  CUlaunchAttribute attr[3];
+  unsigned na = 0;
   if (cluster && (cluster[0] * cluster[1] * cluster[2]) > 1) {
-    attr[0].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
-    attr[0].value.clusterDim.x = cluster[0];
-    attr[0].value.clusterDim.y = cluster[1];
-    attr[0].value.clusterDim.z = cluster[2];
+    attr[na].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+    attr[na].value.clusterDim.x = cluster[0];
+    attr[na].value.clusterDim.y = cluster[1];
+    attr[na].value.clusterDim.z = cluster[2];
+    ++na;
+  }
+  if (flags & RS_LAUNCH_COOPERATIVE) {  // every block co-resident (grid-wide barriers), or the launch fails
+    attr[na].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
+    attr[na].value.cooperative = 1;
+    ++na;
+  }
+  if (flags & RS_LAUNCH_PDL) {
+    attr[na].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[na].value.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (na) {
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
   }
   CU(g_drv.LaunchKernelEx(&cfg, f->fn, args, nullptr), "cuLaunchKernelEx");
   return 0;

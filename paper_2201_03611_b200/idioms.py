@@ -23,7 +23,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
-from . import lir, tmpl_allpairs, tmpl_gemm, tmpl_rowfold, tmpl_seqfold, tmpl_stencil
+from . import lir, tmpl_allpairs, tmpl_gemm, tmpl_iterate, tmpl_rowfold, tmpl_seqfold, tmpl_stencil
 from ._ref import nat
 from .emit_cuda import NatRenderer, ValueRenderer, collapse_global_chain, kernel_head, py_expr
 
@@ -36,7 +36,15 @@ class IdiomKernel:
     includes: list = field(default_factory=list)
 
 
-ORDER_PRESERVING = ("_match_rowfold", "_match_stencil", "_match_seqfold")
+ORDER_PRESERVING = ("_match_rowfold", "_match_stencil", "_match_seqfold", "_match_iterate")
+
+
+def _match_iterate(prog, stage, base_name, temps, exact):
+    out = tmpl_iterate.match(prog, stage, base_name, temps, exact)
+    if out is None:
+        return None
+    text, plan = out
+    return IdiomKernel(plan["name"], text, plan)
 
 
 def _match_seqfold(prog, stage, base_name, temps, exact):
@@ -49,7 +57,7 @@ def _match_seqfold(prog, stage, base_name, temps, exact):
 
 def match(prog, stage, base_name, temps, exact, reassociate=True):
     for matcher in (_match_gemm, _match_rowfold, _match_reduce, _match_stencil, _match_allpairs,
-                    _match_seqfold):
+                    _match_seqfold, _match_iterate):
         if not reassociate and matcher.__name__ not in ORDER_PRESERVING:
             continue
         out = matcher(prog, stage, base_name, temps, exact)
@@ -514,4 +522,5 @@ LAUNCHERS = {
     "allpairs": tmpl_allpairs.launch,
     "gemm_tc": tmpl_gemm.launch,
     "seqfold": tmpl_seqfold.launch,
+    "iterate": tmpl_iterate.launch,
 }

@@ -154,7 +154,7 @@ class Executable:
             args = list(base_args)
             for extra in st.get("extra_args", []):
                 args.append(self._extra_arg(extra, buffers, temps))
-            fn.launch(grid, block, args, smem=smem, stream=stream, cluster=cluster)
+            fn.launch(grid, block, args, smem=smem, stream=stream, cluster=cluster, flags=_launch_flags(st))
 
     def bind(self, buffers: dict, stream=None):
         """Pre-build every launch (argument arrays, tensor maps) for fixed
@@ -174,7 +174,7 @@ class Executable:
         prepared = []
         for st, fn, grid, block, smem, cluster in self.kernels:
             args = list(base_args) + [self._extra_arg(e, buffers, temps) for e in st.get("extra_args", [])]
-            prepared.append(rt.PreparedLaunch(fn, grid, block, args, smem, stream, cluster))
+            prepared.append(rt.PreparedLaunch(fn, grid, block, args, smem, stream, cluster, _launch_flags(st)))
 
         def launch_all():
             for p in prepared:
@@ -332,6 +332,10 @@ class Executable:
         buffers[self.plan["output"]["name"]] = out
         self.launch(buffers, stream=stream if stream is not None else torch.cuda.current_stream())
         return out
+
+
+def _launch_flags(st) -> int:
+    return 1 if st.get("cooperative") else 0  # RS_LAUNCH_COOPERATIVE
 
 
 def _dptr(x):

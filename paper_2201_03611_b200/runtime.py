@@ -29,7 +29,7 @@ EXPORTED = (
     "rs_last_error", "rs_abi_version", "rs_init", "rs_device_count", "rs_device_attribute",
     "rs_nvrtc_version", "rs_compile", "rs_compile_cubin", "rs_free_host", "rs_module_load",
     "rs_module_lowered_name", "rs_module_get_function", "rs_module_unload",
-    "rs_function_attribute", "rs_launch", "rs_malloc", "rs_free", "rs_memcpy_htod",
+    "rs_function_attribute", "rs_launch", "rs_launch_ex", "rs_malloc", "rs_free", "rs_memcpy_htod",
     "rs_memcpy_dtoh", "rs_memcpy_dtod", "rs_memset_d8", "rs_stream_create",
     "rs_stream_destroy", "rs_stream_synchronize", "rs_device_synchronize", "rs_event_create",
     "rs_event_destroy", "rs_event_record", "rs_event_synchronize", "rs_event_elapsed_ms",
@@ -73,6 +73,8 @@ def lib():
             L.rs_function_attribute.argtypes = [vp, i, ctypes.POINTER(i)]
             L.rs_launch.argtypes = [vp, ctypes.POINTER(u), ctypes.POINTER(u), ctypes.POINTER(u),
                                     u, vp, ctypes.POINTER(vp)]
+            L.rs_launch_ex.argtypes = [vp, ctypes.POINTER(u), ctypes.POINTER(u), ctypes.POINTER(u),
+                                       u, vp, ctypes.POINTER(vp), u]
             L.rs_malloc.argtypes = [ctypes.POINTER(vp), sz]
             L.rs_free.argtypes = [vp]
             for name in ("rs_memcpy_htod", "rs_memcpy_dtoh", "rs_memcpy_dtod"):
@@ -228,8 +230,9 @@ class Function:
         check_run(lib().rs_function_attribute(self.handle, attr, ctypes.byref(v)), "rs_function_attribute")
         return v.value
 
-    def launch(self, grid, block, args, smem=0, stream=None, cluster=(1, 1, 1)):
-        """`args`: list of ctypes values (kept alive for the call)."""
+    def launch(self, grid, block, args, smem=0, stream=None, cluster=(1, 1, 1), flags=0):
+        """`args`: list of ctypes values (kept alive for the call); `flags`:
+        RS_LAUNCH_COOPERATIVE (1) / RS_LAUNCH_PDL (2) of rs_launch_ex."""
         g = (ctypes.c_uint * 3)(*_dim3(grid))
         b = (ctypes.c_uint * 3)(*_dim3(block))
         c = (ctypes.c_uint * 3)(*_dim3(cluster))
@@ -237,7 +240,7 @@ class Function:
         for k, a in enumerate(args):
             ptrs[k] = ctypes.cast(ctypes.byref(a), ctypes.c_void_p)
         check_run(
-            lib().rs_launch(self.handle, g, b, c, int(smem), _stream_ptr(stream), ptrs),
+            lib().rs_launch_ex(self.handle, g, b, c, int(smem), _stream_ptr(stream), ptrs, int(flags)),
             f"launch of {self.name}",
         )
 
@@ -245,8 +248,9 @@ class Function:
 class PreparedLaunch:
     """One kernel launch with its argument array built once."""
 
-    def __init__(self, fn: Function, grid, block, args, smem=0, stream=None, cluster=(1, 1, 1)):
+    def __init__(self, fn: Function, grid, block, args, smem=0, stream=None, cluster=(1, 1, 1), flags=0):
         self.fn = fn
+        self.flags = int(flags)
         self.args = list(args)  # keep the ctypes values alive
         self.g = (ctypes.c_uint * 3)(*_dim3(grid))
         self.b = (ctypes.c_uint * 3)(*_dim3(block))
@@ -256,10 +260,10 @@ class PreparedLaunch:
             self.ptrs[k] = ctypes.cast(ctypes.byref(a), ctypes.c_void_p)
         self.smem = int(smem)
         self.stream = _stream_ptr(stream)
-        self._launch = lib().rs_launch
+        self._launch = lib().rs_launch_ex
 
     def __call__(self):
-        if self._launch(self.fn.handle, self.g, self.b, self.c, self.smem, self.stream, self.ptrs) != 0:
+        if self._launch(self.fn.handle, self.g, self.b, self.c, self.smem, self.stream, self.ptrs, self.flags) != 0:
             check_run(1, f"launch of {self.fn.name}")
 
 

@@ -134,3 +134,33 @@ def test_fuse_reduce_map_known_answer(gpu):
                         "fuseReduceMap @ every(isReduce) ; toReduceSeq @ every(isReduce)", name="sumSq")
     out = run_cuda(emit_cuda(c.unit), c.unit, {}, [[1, 2, 3]])
     assert int(np.asarray(out).reshape(-1)[0]) == 14
+
+
+ITERATE_BIG = """
+def pairSum = depFun((n: Nat) => fun(xs: Array[8 * n, f32] =>
+  xs |> iterate(3)(depFun((l: Nat) => fun(a: Array[l * 2, f32] =>
+    a |> split(2) |> mapGlobal(fun(p =>
+      p |> reduceSeq(Private)(fun(acc, v => acc + v))(0.0f) )) ))) ))
+"""
+
+
+@pytest.mark.parametrize("n", [1, 1000, 1 << 20])
+def test_iterate_on_the_whole_gpu(gpu, n):
+    """iterate(3) of a parallel pairwise sum: the `iterate` template keeps
+    the ping-pong buffers in global memory and separates the steps with a
+    grid-wide barrier of a cooperative launch, so sizes far beyond shared
+    memory run; bit-exact with the program's own order."""
+    from paper_2201_03611_b200.run import Executable
+
+    c = compile_program(ITERATE_BIG, None, name="pairSum")
+    code = emit_cuda(c.unit)
+    assert Executable(code, {"n": n}).template_kinds == ["iterate"]
+    xs = np.random.default_rng(n).uniform(-1, 1, 8 * n).astype(np.float32)
+    got = run_cuda(code, c.unit, {"n": n}, [xs], as_numpy=True)
+    want = xs
+    for _ in range(3):  # each step: (0 + a[2g]) + a[2g + 1]
+        want = ((np.float32(0) + want[0::2]) + want[1::2]).astype(np.float32)
+    np.testing.assert_array_equal(got, want)
+    if n <= 1000:  # and the reference's imperative interpreter agrees
+        ref = interpreter.run_unit(c.unit, {"n": n}, [[np.float32(v) for v in xs]])
+        np.testing.assert_array_equal(np.asarray(ref, np.float32), want)

@@ -8,9 +8,12 @@ HBM.  Default workload: BASELINE.json configs[1], gemv fp32 8192x8192
 (`mv.rise` + the toMapGlobal strategy).  Other configs: --workload.
 
 Prints ONE JSON line (rank 0).  Timing: W warm-up steps; K timed steps
-bracketed by barrier + synchronize; each step's kernels timed with CUDA
-events on the launching stream; L2 flushed (256 MiB write) between steps
-outside the events; max over ranks.  `e2e` repeats the step through the
+bracketed by barrier + synchronize, timed with CUDA events on the launching
+stream, max over ranks.  HBM-bound workloads use inputs larger than L2: R
+input sets (>= 3x the L2 in total) round robin, the K steps back to back
+between two events (RISE_BENCH_L2=flush selects the other mode);
+compute-bound ones flush the L2 (256 MiB write + read) before every step,
+outside that step's events.  `e2e` repeats the step through the
 public host-buffer path (pinned H2D, launch, D2H).  `--impl reference`
 times the reference's own CPU implementation (its emitted C/OpenMP,
 oracle/_ref) on this host's cores instead.
@@ -34,6 +37,7 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "oracle"))  # checker / CPU-baseline legs only
 
 L2_FLUSH_BYTES = 256 << 20
+L2_BYTES = 126 << 20  # B200 L2
 FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # derived, BASELINE.md §2
 
 
@@ -391,27 +395,64 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.Stream()
     dev_in = [torch.from_numpy(np.ascontiguousarray(h).reshape(-1)).to("cuda") for h in host]
     out = torch.empty(exe.output_size, dtype=torch.float32, device="cuda")
-    extra = {}
-    peer_sources = None
-    if exe.plan.get("peer_halo"):
-        from paper_2201_03611_b200 import shard
-
-        torch.cuda.synchronize()
-        peer_sources = shard.PeerHaloRows(dev_in[0].view(nats["n"], nats["m"]), exe.plan["stages"][0]["halo_rows"])
-        dist.barrier()
-        extra.update(peer_sources.extra)
-    if exe.plan.get("peer_ranks"):
-        from paper_2201_03611_b200 import shard
-
-        torch.cuda.synchronize()
-        peer_sources = shard.PeerSources({"pos": dev_in[2], "mass": dev_in[3]},
-                                         exe.plan["stages"][0]["peer_streams"])
-        dist.barrier()
-        extra["rs_peer_table"] = peer_sources.table
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
-    sweep = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
-    sink = torch.empty((), dtype=torch.float32, device="cuda")
     n_stages = len(exe.kernels)
+    use_graph = n_stages > 1 and os.environ.get("RISE_BENCH_GRAPH", "1") == "1"
+    keepalive = []  # peer exports of every input set stay open for the run
+
+    def make_step(dev_in, out):
+        """One step's launches on one input set (bound arguments, peer
+        tables and the multi-GPU exchange included)."""
+        extra = {}
+        peer_sources = None
+        if exe.plan.get("peer_halo"):
+            from paper_2201_03611_b200 import shard
+
+            torch.cuda.synchronize()
+            peer_sources = shard.PeerHaloRows(dev_in[0].view(nats["n"], nats["m"]), exe.plan["stages"][0]["halo_rows"])
+            dist.barrier()
+            extra.update(peer_sources.extra)
+        if exe.plan.get("peer_ranks"):
+            from paper_2201_03611_b200 import shard
+
+            torch.cuda.synchronize()
+            peer_sources = shard.PeerSources({"pos": dev_in[2], "mass": dev_in[3]},
+                                             exe.plan["stages"][0]["peer_streams"])
+            dist.barrier()
+            extra["rs_peer_table"] = peer_sources.table
+        keepalive.append(peer_sources)
+        launch = _bound_launch(exe, dev_in, out, stream, extra)
+        if use_graph:
+            # a multi-kernel unit replays as one CUDA graph launch
+            buffers = dict(extra)
+            buffers.update({spec["name"]: value for spec, value in zip(exe.plan["inputs"], dev_in)})
+            buffers[exe.plan["output"]["name"]] = out
+            launch = exe.graph(buffers, stream)
+        if world > 1 and not peer_sources:
+            return _distributed_step(wl, exe, dev_in, out, stream, dist, rank, world), extra, peer_sources
+        return launch, extra, peer_sources
+
+    step, extra, peer_sources = make_step(dev_in, out)
+
+    # L2 policy between timed steps.  HBM-bound workloads: inputs larger than
+    # L2 — R input sets (>= 3x L2 in total) used round robin, so every step
+    # reads data evicted by the R - 1 sets read since, and the K steps run
+    # back to back between two events.  The others: the L2 is flushed
+    # (written, then a second buffer read) before each step, outside its events.
+    set_bytes = 4 * (sum(t.numel() for t in dev_in) + out.numel())
+    rotate = wl.bound == "hbm" and os.environ.get("RISE_BENCH_L2", "rotate") == "rotate"
+    if rotate:
+        n_sets = max(2, -(-3 * L2_BYTES // set_bytes))
+        steps = [step]
+        for _ in range(n_sets - 1):
+            d_in = [t.clone() for t in dev_in]
+            steps.append(make_step(d_in, torch.empty_like(out))[0])
+        l2_text = (f"inputs larger than L2: {n_sets} input sets of {set_bytes / 2**20:.0f} MiB "
+                   f"(>= 3x the {L2_BYTES >> 20} MiB L2) used round robin, steps back to back")
+    else:
+        flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+        sweep = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+        sink = torch.empty((), dtype=torch.float32, device="cuda")
+        l2_text = "flushed between steps (256 MiB write + 256 MiB read sweep, outside the events)"
 
     def flush_l2():
         # write a buffer larger than L2, then read another one so the dirty
@@ -419,43 +460,42 @@ def run_ours(args, rank, world, local_rank):
         flush.zero_()
         torch.sum(sweep, dim=0, out=sink)
 
-    launch = _bound_launch(exe, dev_in, out, stream, extra)
-    if n_stages > 1 and os.environ.get("RISE_BENCH_GRAPH", "1") == "1":
-        # a multi-kernel unit replays as one CUDA graph launch
-        buffers = dict(extra)
-        buffers.update({spec["name"]: value for spec, value in zip(exe.plan["inputs"], dev_in)})
-        buffers[exe.plan["output"]["name"]] = out
-        launch = exe.graph(buffers, stream)
-
-    def step():
-        launch()
-
-    if world > 1 and not peer_sources:
-        step = _distributed_step(wl, exe, dev_in, out, stream, dist, rank, world)
-
     with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            flush_l2()
-            step()
+        for i in range(args.warmup):
+            if rotate:
+                steps[i % len(steps)]()
+            else:
+                flush_l2()
+                step()
     torch.cuda.synchronize()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clocks:
-        for s in range(args.steps):
+        if rotate:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             with torch.cuda.stream(stream):
-                flush_l2()
-                starts[s].record(stream)
-                step()
-                ends[s].record(stream)
+                e0.record(stream)
+                for s_ in range(args.steps):
+                    steps[(args.warmup + s_) % len(steps)]()
+                e1.record(stream)
+        else:
+            starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+            ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+            for s_ in range(args.steps):
+                with torch.cuda.stream(stream):
+                    flush_l2()
+                    starts[s_].record(stream)
+                    step()
+                    ends[s_].record(stream)
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
-    per_step = [starts[s].elapsed_time(ends[s]) for s in range(args.steps)]
-    total_ms = float(sum(per_step))
+    if rotate:
+        total_ms = float(e0.elapsed_time(e1))
+    else:
+        total_ms = float(sum(starts[s_].elapsed_time(ends[s_]) for s_ in range(args.steps)))
     if dist is not None:
         t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -521,7 +561,7 @@ def run_ours(args, rank, world, local_rank):
                 "sizes": nats,
                 "kernels": exe.kernel_names,
                 "templates": exe.template_kinds,
-                "l2": "flushed between steps (256 MiB write + 256 MiB read sweep, outside the events)",
+                "l2": l2_text,
                 "launch": ("one CUDA graph per step (Executable.graph)" if n_stages > 1
                            and os.environ.get("RISE_BENCH_GRAPH", "1") == "1" else "direct rs_launch per kernel"),
                 "parallelism": _parallelism_text(wl, world) + (
@@ -543,9 +583,10 @@ def run_ours(args, rank, world, local_rank):
         }
     if dist is not None:
         dist.barrier()
-        if peer_sources is not None:
-            peer_sources.close()
-            dist.barrier()
+        for ps in keepalive:
+            if ps is not None:
+                ps.close()
+        dist.barrier()
         dist.destroy_process_group()
     return result
 
@@ -626,6 +667,18 @@ def _bound_launch(exe, dev_in, out, stream, extra=None):
     return exe.bind(buffers, stream)
 
 
+_COMM = []
+
+
+def _device_comm():
+    """One NCCL communicator per process, shared by every input set's step."""
+    if not _COMM:
+        from paper_2201_03611_b200 import shard
+
+        _COMM.append(shard.DeviceComm())
+    return _COMM[0]
+
+
 def _distributed_step(wl, exe, dev_in, out, stream, dist, rank, world):
     import torch
 
@@ -644,9 +697,7 @@ def _distributed_step(wl, exe, dev_in, out, stream, dist, rank, world):
     native = dist.get_backend() == "nccl"
     comm = None
     if native and wl.key in ("dot", "dot_chunked", "nbody"):
-        from paper_2201_03611_b200 import shard
-
-        comm = shard.DeviceComm()
+        comm = _device_comm()
     if wl.key in ("dot", "dot_chunked"):
         parts = [torch.empty(1, dtype=torch.float32, device="cuda") for _ in range(world)]
         flat = torch.empty(world, dtype=torch.float32, device="cuda")

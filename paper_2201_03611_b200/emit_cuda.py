@@ -37,6 +37,7 @@ semantics (interpreter.py:161-169).
 from __future__ import annotations
 
 import json
+import os
 from dataclasses import dataclass, field
 
 from . import lir
@@ -522,6 +523,24 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, pee
                     includes.append(inc)
             entry = dict(match.plan, fallback=generic.plan)
         plan_stages.append(entry)
+    if PDL and len(stages) > 1:
+        # programmatic dependent launch: stage k > 0 may be scheduled while
+        # stage k - 1 drains; its first act is to wait for that grid's
+        # completion and memory (a no-op when launched without the attribute)
+        for k in range(1, len(plan_stages)):
+            for st_plan in (plan_stages[k], plan_stages[k].get("fallback")):
+                if st_plan:
+                    st_plan["pdl"] = True
+        def names(stage_plans):
+            return [p["name"] for p in stage_plans] + [p["fallback"]["name"] for p in stage_plans if p.get("fallback")]
+        # every stage but the last lets its dependent be scheduled at once: the
+        # dependent's wait still covers this grid's completion and memory
+        kernels = [_pdl_insert(kt, names(plan_stages[:-1]), "griddepcontrol.launch_dependents;",
+                               "PDL: the next stage may be scheduled")
+                   for kt in kernels]
+        kernels = [_pdl_insert(kt, names(plan_stages[1:]), "griddepcontrol.wait;",
+                               "PDL: the previous stage is done")
+                   for kt in kernels]
     plan = {
         "version": 1,
         "target": TARGET,
@@ -550,6 +569,21 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, pee
     ] + [f"#include <{inc}>" for inc in includes]
     text = "\n".join(header) + "\n\n" + "\n".join(kernels)
     return CudaCode(text, plan, prog)
+
+
+PDL = os.environ.get("RISE_PDL", "1") == "1"
+
+
+def _pdl_insert(text, names, insn, why):
+    """Insert the PTX `insn` as the first statement of the kernels named in
+    `names` (their `__global__ ... name(...) {` line)."""
+    out = []
+    for line in text.split("\n"):
+        out.append(line)
+        if line.startswith("__global__") and line.rstrip().endswith("{") and \
+                any(f" {n}(" in line for n in names):
+            out.append(f'  asm volatile("{insn}" ::: "memory");  // {why}')
+    return "\n".join(out)
 
 
 def _prod(dims):

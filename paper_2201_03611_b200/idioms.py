@@ -202,8 +202,9 @@ def _launch_rowfold(st, nats, sm):
     from .emit_cuda import eval_py
 
     rows = eval_py(st["rows"], nats)
-    grid = max(1, -(-rows // st["row_block"]))
-    return (grid, 1, 1), (st["row_block"], 1, 1), st["smem"], (1, 1, 1)
+    rb = eval_py(str(st["row_block"]), nats)
+    grid = max(1, -(-rows // rb))
+    return (grid, 1, 1), (rb, 1, 1), eval_py(str(st["smem"]), nats), (1, 1, 1)
 
 
 # ---------------------------------------------------------------------------

@@ -200,7 +200,8 @@ class Executable:
             base += 4 * eval_py(extra.get("offset", "0"), self.nats)
             dims = [eval_py(d, self.nats) for d in extra["dims"]]
             pitch = eval_py(extra.get("pitch", extra["dims"][0]), self.nats)
-            return rt.tma_desc_2d_f32(base, dims[0], dims[1], pitch * 4, extra["box"][0], extra["box"][1],
+            box = [eval_py(str(b), self.nats) for b in extra["box"]]
+            return rt.tma_desc_2d_f32(base, dims[0], dims[1], pitch * 4, box[0], box[1],
                                       extra.get("swizzle", 0))
         if kind == "peer_ptr":  # optional: absent / None / 0 -> NULL (e.g. the image's real edge)
             value = buffers.get(extra["name"])
@@ -335,7 +336,7 @@ class Executable:
 
 
 def _launch_flags(st) -> int:
-    return 1 if st.get("cooperative") else 0  # RS_LAUNCH_COOPERATIVE
+    return (1 if st.get("cooperative") else 0) | (2 if st.get("pdl") else 0)  # RS_LAUNCH_COOPERATIVE | _PDL
 
 
 def _dptr(x):

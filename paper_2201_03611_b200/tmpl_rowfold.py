@@ -23,7 +23,7 @@ chunk c ^ (l & 7): conflict-free LDS.128.  Shared streams arrive by 1-D bulk
 copy.  One elected lane arms the stage's mbarrier with the expected bytes and
 issues every copy (a handful of TMA instructions per stage instead of one
 bulk copy per row); the warp consumes stage t while stages t+1.. are in
-flight.  Block = one warp = 32 rows.
+flight.  Block = one warp = 32 rows (16 or 8 for short matrices: rows_per_block).
 """
 
 from __future__ import annotations
@@ -32,12 +32,29 @@ from . import lir
 from ._ref import nat
 from .emit_cuda import NatRenderer, ValueRenderer, kernel_head, py_expr
 
-ROWS = 32
 import os  # noqa: E402
+
+ROWS = int(os.environ.get("RISE_ROWFOLD_ROWS", "0"))  # rows per block (8, 16 or 32); 0 = by row count
 
 KT = int(os.environ.get("RISE_ROWFOLD_KT", "256"))  # columns per stage (KT/32 TMA boxes of 32 columns)
 STAGES = int(os.environ.get("RISE_ROWFOLD_STAGES", "2"))  # measured (gemv 8192²): 128x6 0.835, 256x2 0.855, 512x2 0.65
-BOX_BYTES = 32 * 32 * 4
+SM_COUNT = 148
+
+
+def rows_per_block(nrows_py):
+    """Rows per block as (Python expression of the sizes, C expression of
+    RS_NROWS).
+
+    One lane folds one row, so a short, wide matrix (the chunked dot's 4096
+    chunks of 4096) leaves too few warps per SM to hide the shared-memory
+    latency of the fold; such shapes get 16 or 8 rows per block, i.e. at
+    least two blocks per SM (boxes of [R rows x 32 floats], same swizzle:
+    its pattern repeats every 8 rows)."""
+    if ROWS:
+        return str(ROWS), str(ROWS)
+    t32, t16 = (2 * SM_COUNT - 1) * 32, (2 * SM_COUNT - 1) * 16
+    return (f"(32 if ({nrows_py}) > {t32} else (16 if ({nrows_py}) > {t16} else 8))",
+            f"(RS_NROWS > {t32} ? 32 : RS_NROWS > {t16} ? 16 : 8)")
 
 
 def affine_in_flat_row(base, loops, assumptions):
@@ -80,6 +97,7 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
     for _, b in loops:
         nrows = nrows * b
     nrows = nat.normalize(nrows, prog.assumptions)
+    rows_py, rows_c = rows_per_block(py_expr(nrows))
 
     rs_list = list(dict.fromkeys(row_streams.values()))
     sh_list = list(dict.fromkeys(shared_streams.values()))
@@ -93,26 +111,27 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
         c0, pitch, apre = aff
         pre += apre + [f"({py_expr(c0)}) % 4 == 0", f"({py_expr(pitch)}) % 4 == 0", f"({py_expr(pitch)}) > 0"]
         tmaps.append({"kind": "tma2d", "buf": buf, "offset": py_expr(c0), "dims": [py_expr(loop.bound), py_expr(nrows)],
-                      "pitch": py_expr(pitch), "box": [32, ROWS], "swizzle": 3})
+                      "pitch": py_expr(pitch), "box": [32, rows_py], "swizzle": 3})
     for buf, base in sh_list:
         pre.append(f"({py_expr(base)}) % 4 == 0")
     pre = list(dict.fromkeys(pre))
 
     nbox = KT // 32
-    stage_floats = len(rs_list) * nbox * 32 * ROWS + len(sh_list) * KT
-    stage_floats = -(-stage_floats // 256) * 256  # stages stay 1024-byte aligned (128B swizzle)
+    # stages stay 1024-byte aligned (128B swizzle)
+    stage_py = f"(-(-({len(rs_list) * nbox * 32} * {rows_py} + {len(sh_list) * KT}) // 256) * 256)"
     extra = [f"const __grid_constant__ rs_tmap rs_map{k}" for k in range(len(rs_list))]
-    lines = kernel_head(prog, name, temps, launch_bounds=ROWS, extra_params=extra)
+    lines = kernel_head(prog, name, temps, launch_bounds=32, extra_params=extra)
     lines += [
-        f"  constexpr int RS_ROWS = {ROWS}, RS_KT = {KT}, RS_STAGES = {STAGES}, RS_NBOX = {nbox};",
         f"  constexpr int RS_NROWS = {r(nrows)};",
+        f"  constexpr int RS_ROWS = {rows_c}, RS_KT = {KT}, RS_STAGES = {STAGES}, RS_NBOX = {nbox};",
+        "  constexpr unsigned RS_MASK = RS_ROWS == 32 ? 0xffffffffu : (1u << RS_ROWS) - 1u;",
         f"  constexpr int RS_K = {r(loop.bound)};",
         "  constexpr int RS_NT = (RS_K + RS_KT - 1) / RS_KT;",
-        f"  constexpr int RS_STAGE_FLOATS = {stage_floats};",
+        f"  constexpr int RS_STAGE_FLOATS = ({len(rs_list) * nbox * 32} * RS_ROWS + {len(sh_list) * KT} + 255) / 256 * 256;",
         "  extern __shared__ __align__(1024) unsigned char rs_smem_raw[];",
         "  float* rs_smem = reinterpret_cast<float*>(rs_smem_raw + ((1024u - (rs_smem_addr(rs_smem_raw) & 1023u)) & 1023u));",
         "  unsigned long long* rs_bar = reinterpret_cast<unsigned long long*>(rs_smem + RS_STAGES * RS_STAGE_FLOATS);",
-        "  const int rs_lane = threadIdx.x;",
+        "  const int rs_lane = threadIdx.x;  // the block is RS_ROWS lanes of one warp",
         "  const int rs_row0 = blockIdx.x * RS_ROWS;",
         "  const bool rs_active = rs_row0 + rs_lane < RS_NROWS;",
         "  const int rs_f = rs_active ? rs_row0 + rs_lane : RS_NROWS - 1;",
@@ -142,7 +161,7 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
         "    for (int rs_s = 0; rs_s < RS_STAGES; ++rs_s) rs_mbar_init(&rs_bar[rs_s], 1);",
         "    rs_fence_barrier_init();",
         "  }",
-        "  __syncwarp();",
+        "  __syncwarp(RS_MASK);",
         "  auto rs_issue = [&](int rs_t) {",
         "    const int rs_slot = rs_t % RS_STAGES;",
         "    const int rs_j0 = rs_t * RS_KT;",
@@ -151,7 +170,7 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
         "    float* rs_st = rs_smem + rs_slot * RS_STAGE_FLOATS;",
         "    rs_fence_proxy_async();",
         "    if (rs_lane == 0) {",
-        f"      rs_mbar_arrive_expect_tx(&rs_bar[rs_slot], (unsigned)(rs_nb * {BOX_BYTES} * {len(rs_list)}"
+        f"      rs_mbar_arrive_expect_tx(&rs_bar[rs_slot], (unsigned)(rs_nb * 128 * RS_ROWS * {len(rs_list)}"
         f" + rs_kt * 4 * {len(sh_list)}));",
     ]
     for k in range(len(rs_list)):
@@ -220,7 +239,7 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
     lines += [
         "      }",
         "    }",
-        "    __syncwarp();",
+        "    __syncwarp(RS_MASK);",
         "  }",
         "  if (rs_active) {",
     ]
@@ -230,12 +249,12 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
         g = GenericKernel(prog, Stage("serial", s), "_", [], exact)
         lines += [("    " + x) for x in g.thread(s, 0)]
     lines += ["  }", "}"]
-    smem = STAGES * stage_floats * 4 + STAGES * 8 + 1024
+    smem = f"{STAGES} * {stage_py} * 4 + {STAGES * 8 + 1024}"
     plan = {
         "name": name,
         "kind": "rowfold",
         "rows": py_expr(nrows),
-        "row_block": ROWS,
+        "row_block": rows_py,
         "smem": smem,
         "pre": pre,
         "fmad": False,

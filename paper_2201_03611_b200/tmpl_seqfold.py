@@ -13,7 +13,8 @@ streams 2048-element tiles of every stream into a 3-stage shared-memory ring
 with 1-D bulk copies (TMA; the next tiles are in flight while the current
 one is folded, and the lane never waits on a global load) and runs the
 program's own step expression over float4 reads of shared memory, so the
-chain advances at the FADD latency.  Order: PRESERVED (bit-exact).
+chain advances at the FADD latency (full tiles: a register pipeline loads
+the next 16 elements while the current 16 are folded).  Order: PRESERVED (bit-exact).
 """
 
 from __future__ import annotations
@@ -73,7 +74,8 @@ def match(prog, stage, base_name, temps, exact, fold_shape, j_coefficient, threa
         f"  constexpr int RS_K = {r(loop.bound)};",
         f"  constexpr int RS_TILE = {max(256, TILE // ns)}, RS_S = {STAGES}, RS_NS = {ns};",
         "  constexpr int RS_NT = (RS_K + RS_TILE - 1) / RS_TILE;",
-        "  __shared__ __align__(128) float rs_ring[RS_S][RS_NS][RS_TILE];",
+        "  // +16: the register pipeline below reads one group past a full tile (never used)",
+        "  __shared__ __align__(128) float rs_ring[RS_S][RS_NS][RS_TILE + 16];",
         "  __shared__ __align__(8) unsigned long long rs_bar[RS_S];",
     ]
     for k, (buf, base) in enumerate(s_list):
@@ -106,6 +108,34 @@ def match(prog, stage, base_name, temps, exact, fold_shape, j_coefficient, threa
         "    const int rs_j0 = rs_t * RS_TILE;",
         "    const int rs_n4 = RS_K4 - rs_j0 < RS_TILE ? (RS_K4 - rs_j0 > 0 ? RS_K4 - rs_j0 : 0) : RS_TILE;",
         "    if (rs_n4 > 0) rs_mbar_wait(&rs_bar[rs_q], (unsigned)((rs_t / RS_S) & 1));",
+        "    if (rs_n4 == RS_TILE) {",
+        "      // full tile: the next 16 elements of every stream are loaded while the",
+        "      // current 16 are folded, so the chain never waits on shared memory",
+    ]
+    ld = "*reinterpret_cast<const float4*>(&rs_ring[rs_q][{k}][{i}])"
+    for k in range(ns):
+        for u in range(4):
+            lines.append(f"      float4 rs_c{k}_{u} = {ld.format(k=k, i=4 * u)};")
+    lines += [
+        "#pragma unroll 2",
+        "      for (int rs_jj = 0; rs_jj < RS_TILE; rs_jj += 16) {",
+    ]
+    for k in range(ns):
+        for u in range(4):
+            lines.append(f"        const float4 rs_n{k}_{u} = {ld.format(k=k, i=f'rs_jj + {16 + 4 * u}')};")
+    for u in range(4):
+        lines.append("        {")
+        for k in range(ns):
+            lines.append(f"          const float4 rs_v{k} = rs_c{k}_{u};")
+        for comp in ("x", "y", "z", "w"):
+            lines.append(f"          {acc.name} = {step_with(comp)};")
+        lines.append("        }")
+    for k in range(ns):
+        for u in range(4):
+            lines.append(f"        rs_c{k}_{u} = rs_n{k}_{u};")
+    lines += [
+        "      }",
+        "    } else {",
         "#pragma unroll 4",
         "    for (int rs_jj = 0; rs_jj < rs_n4; rs_jj += 4) {",
     ]
@@ -114,6 +144,7 @@ def match(prog, stage, base_name, temps, exact, fold_shape, j_coefficient, threa
     for comp in ("x", "y", "z", "w"):
         lines.append(f"      {acc.name} = {step_with(comp)};")
     lines += [
+        "    }",
         "    }",
         "  }",
         "  for (int rs_j = RS_K4; rs_j < RS_K; ++rs_j) {  // K % 4 tail, straight from global memory",

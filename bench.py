@@ -10,7 +10,7 @@ HBM.  Default workload: BASELINE.json configs[1], gemv fp32 8192x8192
 Prints ONE JSON line (rank 0).  Timing: W warm-up steps; K timed steps
 bracketed by barrier + synchronize, timed with CUDA events on the launching
 stream, max over ranks.  HBM-bound workloads use inputs larger than L2: R
-input sets (>= 3x the L2 in total) round robin, the K steps back to back
+input sets (>= 512 MiB, 4x the L2, in total) round robin, the K steps back to back
 between two events (RISE_BENCH_L2=flush selects the other mode);
 compute-bound ones flush the L2 (256 MiB write + read) before every step,
 outside that step's events.  `e2e` repeats the step through the
@@ -38,6 +38,7 @@ sys.path.insert(0, str(ROOT / "oracle"))  # checker / CPU-baseline legs only
 
 L2_FLUSH_BYTES = 256 << 20
 L2_BYTES = 126 << 20  # B200 L2
+ROTATE_BYTES = 512 << 20  # input sets used round robin cover >= 4x L2
 FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # derived, BASELINE.md §2
 
 
@@ -434,20 +435,20 @@ def run_ours(args, rank, world, local_rank):
     step, extra, peer_sources = make_step(dev_in, out)
 
     # L2 policy between timed steps.  HBM-bound workloads: inputs larger than
-    # L2 — R input sets (>= 3x L2 in total) used round robin, so every step
+    # L2 — R input sets (>= 512 MiB = 4x L2 in total) used round robin, so every step
     # reads data evicted by the R - 1 sets read since, and the K steps run
     # back to back between two events.  The others: the L2 is flushed
     # (written, then a second buffer read) before each step, outside its events.
     set_bytes = 4 * (sum(t.numel() for t in dev_in) + out.numel())
     rotate = wl.bound == "hbm" and os.environ.get("RISE_BENCH_L2", "rotate") == "rotate"
     if rotate:
-        n_sets = max(2, -(-3 * L2_BYTES // set_bytes))
+        n_sets = int(os.environ.get("RISE_BENCH_SETS", "0")) or max(2, -(-ROTATE_BYTES // set_bytes))
         steps = [step]
         for _ in range(n_sets - 1):
             d_in = [t.clone() for t in dev_in]
             steps.append(make_step(d_in, torch.empty_like(out))[0])
         l2_text = (f"inputs larger than L2: {n_sets} input sets of {set_bytes / 2**20:.0f} MiB "
-                   f"(>= 3x the {L2_BYTES >> 20} MiB L2) used round robin, steps back to back")
+                   f"(>= 512 MiB, 4x the {L2_BYTES >> 20} MiB L2) used round robin, steps back to back")
     else:
         flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
         sweep = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")

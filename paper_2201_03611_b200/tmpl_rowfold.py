@@ -48,11 +48,13 @@ def rows_per_block(nrows_py):
     One lane folds one row, so a short, wide matrix (the chunked dot's 4096
     chunks of 4096) leaves too few warps per SM to hide the shared-memory
     latency of the fold; such shapes get 16 or 8 rows per block, i.e. at
-    least two blocks per SM (boxes of [R rows x 32 floats], same swizzle:
+    least one block per SM (boxes of [R rows x 32 floats], same swizzle:
     its pattern repeats every 8 rows)."""
     if ROWS:
         return str(ROWS), str(ROWS)
-    t32, t16 = (2 * SM_COUNT - 1) * 32, (2 * SM_COUNT - 1) * 16
+    # measured (B200): gemv 8192 rows 32 > 16 (0.864 / 0.849); chunked dot
+    # 4096 rows 16 = 32 > 8 — keep 32 until it leaves SMs without a block
+    t32, t16 = SM_COUNT * 32, SM_COUNT * 16
     return (f"(32 if ({nrows_py}) > {t32} else (16 if ({nrows_py}) > {t16} else 8))",
             f"(RS_NROWS > {t32} ? 32 : RS_NROWS > {t16} ? 16 : 8)")
 

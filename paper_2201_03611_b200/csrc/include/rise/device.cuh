@@ -131,6 +131,14 @@ RS_DEVICE void rs_tma_store_2d(const rs_tmap* map, int c0, int c1, const void* s
                "r"(c0), "r"(c1), "r"(rs_smem_addr(src))
                : "memory");
 }
+// 1-D bulk copy shared -> global (16-byte aligned, size a multiple of 16),
+// tracked as a bulk async-group of the issuing thread.
+RS_DEVICE void rs_bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                   reinterpret_cast<unsigned long long>(dst)),
+               "r"(rs_smem_addr(src)), "r"(bytes)
+               : "memory");
+}
 RS_DEVICE void rs_bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // the shared-memory sources of every committed bulk store have been read
 RS_DEVICE void rs_bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }

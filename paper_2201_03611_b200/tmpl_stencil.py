@@ -13,12 +13,15 @@ round-to-nearest intrinsics); only the loads of A are redirected.
 Bit-identical to the reference's semantics.
 
 Data movement:
-* a block computes a TR x TC = 64 x 128 output tile (32 x 8 threads, each
-  thread RPT = 8 rows x CPT = 4 adjacent columns);
+* a block computes a TR x TC = 32 x 256 output tile (64 x 4 threads, each
+  thread RPT = 8 rows x CPT = 4 adjacent columns; 1-KiB row segments keep
+  the DRAM streams long: 0.80 of the copy peak against 0.77 for 64 x 128);
 * the tile's input footprint (rows + halo, columns + halo, left edge padded
-  to a 16-byte boundary) is staged into shared memory by ONE 2-D TMA load
-  for interior tiles; border tiles stage through clamped loads (padClamp
-  semantics), so no per-access clamp remains in the compute;
+  to a 16-byte boundary) is staged into shared memory by the bulk-copy
+  engine: ONE 2-D TMA load when a staged row fits a TMA box (<= 256
+  elements), else one 1-D bulk copy per staged row (`rowcopy`, the default
+  264-column footprint); border tiles then get the padClamp values by an
+  in-shared-memory fix-up, so no per-access clamp remains in the compute;
 * each thread copies its (RPT + halo) x (CPT + halo) window from shared
   memory into registers (LDS.128 for the aligned middle columns), and the
   body's loads of A become constant-indexed register reads after unrolling
@@ -33,15 +36,19 @@ from .emit_cuda import GenericKernel, NatRenderer, Stage, ValueRenderer, kernel_
 
 import os  # noqa: E402
 
-TX = 32  # threads along a row (one warp: 16-byte stores of adjacent columns)
-TY = int(os.environ.get("RISE_STENCIL_TY", "8"))
+# threads along a row (4 adjacent columns each).  Measured (8192², 3 blocks
+# per SM, round-robin inputs): 32 -> 64 x 128 tiles 0.77, 64 -> 32 x 256
+# tiles 0.80, 128 -> 16 x 512 tiles 0.75 (the row halo grows)
+TX = int(os.environ.get("RISE_STENCIL_TX", "64"))
+TY = int(os.environ.get("RISE_STENCIL_TY", str(256 // TX)))
 RPT = int(os.environ.get("RISE_STENCIL_RPT", "8"))  # output rows per thread
 CPT = 4  # adjacent output columns per thread
 TR, TC = TY * RPT, TX * CPT
 
 # persistent blocks per SM (each holds two 36 KB stages); overridable for sweeps
 BLOCKS_PER_SM = int(os.environ.get("RISE_STENCIL_BPS", "3"))
-# full tiles leave through shared memory and one TMA tile store (else 16-byte STGs)
+# full tiles leave through shared memory and one TMA tile store, or one bulk
+# store per row in rowcopy mode (else 16-byte STGs)
 TMA_STORE = os.environ.get("RISE_STENCIL_TMA_STORE", "1") == "1"
 STAGES = int(os.environ.get("RISE_STENCIL_STAGES", "2"))  # ring depth per block (measured: 2 x 3 blocks/SM 0.82 > 3 x 2 0.78 > 4 x 1 0.77)
 
@@ -129,6 +136,9 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     lp = -(-hcl // 4) * 4  # left pad, keeps the thread's columns 16-byte aligned
     sw = -(-(lp + TC + hcr) // 4) * 4  # staged row width (multiple of 16 bytes)
     sr = TR + hr  # staged rows
+    # staged rows wider than a TMA box (<= 256 elements) arrive as one 1-D
+    # bulk copy per row and leave as one bulk store per row
+    rowcopy = sw > 256 or os.environ.get("RISE_STENCIL_ROWCOPY", "0") == "1"
     wr, wc = RPT + hr, CPT + hcl + hcr  # register window
 
     # small row/column-invariant inputs (e.g. the 3x3 weights) live in registers
@@ -158,12 +168,12 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     g = GenericKernel(prog, Stage("serial", body), "_", [], exact)
     g.r = ValueRenderer(prog, exact, load_hook=hook)
     body_lines = g.thread(body, 4)
-    pair_lines, store_pre, ostore = _pair_body(prog, body, rv, cv, abuf, small, hook, exact, r, TMA_STORE)
+    pair_lines, store_pre, ostore = _pair_body(prog, body, rv, cv, abuf, small, hook, exact, r, TMA_STORE, rowcopy)
     tma_store = ostore is not None
     hdim = r(nat.normalize(A.dims[0] - nat.Const(1)))
     wdim = r(nat.normalize(A.dims[1] - nat.Const(1)))
-    params = ["const __grid_constant__ rs_tmap rs_map"]
-    if tma_store:
+    params = [] if rowcopy else ["const __grid_constant__ rs_tmap rs_map"]
+    if tma_store and not rowcopy:
         params.append("const __grid_constant__ rs_tmap rs_omap")
     peer_halo = bool(getattr(prog, "peer_halo", False))
     ht, hb = -o0lo, o0hi  # rows of halo above / below the band
@@ -210,8 +220,19 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "    int r0, c0;",
         "    rs_origin(t, r0, c0);",
         "    rs_fence_proxy_async();  // earlier generic-proxy accesses of this stage precede the TMA write",
+    ] + ([
         "    rs_mbar_arrive_expect_tx(&rs_bar[s], (unsigned)(RS_SR * RS_SW * 4));",
         f"    rs_tma_load_2d(rs_buf + s * RS_STAGE, &rs_map, c0 - {lp}, r0 + ({o0lo}), &rs_bar[s]);",
+    ] if not rowcopy else [
+        "    // one bulk copy per staged row, in-range cells only (the clamp fix-up fills the rest)",
+        f"    const int tr0 = r0 + ({o0lo}), tc0 = c0 - {lp};",
+        "    const int cs = tc0 < 0 ? 0 : tc0, ce = tc0 + RS_SW > RS_W ? RS_W : tc0 + RS_SW;",
+        "    const int ys = tr0 < 0 ? -tr0 : 0, ye = tr0 + RS_SR > RS_H ? RS_H - tr0 : RS_SR;",
+        "    rs_mbar_arrive_expect_tx(&rs_bar[s], (unsigned)((ye - ys) * (ce - cs) * 4));",
+        "    for (int y = ys; y < ye; ++y)",
+        f"      rs_bulk_g2s(rs_buf + s * RS_STAGE + y * RS_SW + (cs - tc0), {abuf} + (tr0 + y) * RS_W + cs,",
+        "                  (unsigned)((ce - cs) * 4), &rs_bar[s]);",
+    ]) + [
         "  };",
         "  if (rs_tid == 0) {",
         "    for (int rs_q = 0; rs_q < RS_NSTAGE; ++rs_q) rs_mbar_init(&rs_bar[rs_q], 1);",
@@ -319,24 +340,26 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "order": "preserved",
         "pre": [f"({py_expr(A.dims[1])}) % 4 == 0", f"({py_expr(R)}) * ({py_expr(C)}) > 0"] + store_pre,
         "packed": pair_lines is not None,
-        "extra_args": [{"kind": "tma2d", "buf": abuf, "offset": "0",
-                        "dims": [py_expr(A.dims[1]), py_expr(A.dims[0])], "pitch": py_expr(A.dims[1]),
-                        "box": [sw, sr], "swizzle": 0}],
+        "extra_args": [] if rowcopy else [{"kind": "tma2d", "buf": abuf, "offset": "0",
+                                           "dims": [py_expr(A.dims[1]), py_expr(A.dims[0])],
+                                           "pitch": py_expr(A.dims[1]), "box": [sw, sr], "swizzle": 0}],
     }
-    if tma_store:
+    if rowcopy:
+        plan["rowcopy"] = True
+    if tma_store and not rowcopy:
         row_coef, const = ostore
         plan["extra_args"].append({"kind": "tma2d", "buf": prog.output.name, "offset": py_expr(const),
                                    "dims": [py_expr(C), py_expr(R)], "pitch": py_expr(row_coef),
                                    "box": [TC, TR], "swizzle": 0})
         plan["tma_store"] = True
-    if peer_halo:  # (kernel parameter order: rs_map, [rs_omap], rs_halo_top, rs_halo_bot)
+    if peer_halo:  # (kernel parameter order: [rs_map, [rs_omap]], rs_halo_top, rs_halo_bot)
         plan["peer_halo"] = True
         plan["halo_rows"] = [ht, hb]
         plan["extra_args"] += [{"kind": "peer_ptr", "name": "rs_halo_top"}, {"kind": "peer_ptr", "name": "rs_halo_bot"}]
     return "\n".join(lines) + "\n", plan
 
 
-def _pair_body(prog, body, rv, cv, abuf, small, hook, exact, r, tma_store):
+def _pair_body(prog, body, rv, cv, abuf, small, hook, exact, r, tma_store, rowcopy=False):
     """Packed fp32x2 version of the body for output columns (q, q + 1):
     (lines of the full-tile compute, extra preconditions, (row pitch, offset)
     of the output when it leaves by TMA store else None), or (None, [], None)."""
@@ -400,7 +423,12 @@ def _pair_body(prog, body, rv, cv, abuf, small, hook, exact, r, tma_store):
             "    rs_fence_proxy_async();  // the generic-proxy writes precede the TMA read",
             "    __syncthreads();",
             "    if (rs_tid == 0) {",
+        ] + ([
             "      rs_tma_store_2d(&rs_omap, rs_c0, rs_r0, rs_tile);",
+        ] if not rowcopy else [
+            f"      for (int rs_y = 0; rs_y < {TR}; ++rs_y)  // one bulk store per output row",
+            f"        rs_bulk_s2g({out} + ({r(const)}) + (rs_r0 + rs_y) * ({r(row_coef)}) + rs_c0, rs_tile + rs_y * {TC}, {TC * 4}u);",
+        ]) + [
             "      rs_bulk_commit();",
             "    }",
         ]

@@ -15,10 +15,10 @@ sys.path.insert(0, str(ROOT))
 
 SRC = r"""
 #include <rise/device.cuh>
-template <int H, int W, int TR, int TC, int NB, int NSTAGE>
+template <int H, int W, int TR, int TC, int NB, int NSTAGE, int PAD, int MODE>
 __global__ void __launch_bounds__(256) tilecopy(float* out, const __grid_constant__ rs_tmap map,
                                                 const __grid_constant__ rs_tmap omap) {
-  constexpr int SR = TR + 2, SW = TC + 8, BW = SW / NB;
+  constexpr int SR = TR + 2, SW = TC + 2 * PAD, BW = SW / NB;  // MODE 0 copy, 1 loads only, 2 stores only
   constexpr int BS = (SR * BW + 31) / 32 * 32;  // box regions stay 128-byte aligned
   constexpr int STAGE = NB * BS;
   constexpr int NTX = W / TC, NTILES = NTX * (H / TR);
@@ -29,9 +29,10 @@ __global__ void __launch_bounds__(256) tilecopy(float* out, const __grid_constan
   auto issue = [&](int t, int s) {
     const int r0 = (t / NTX) * TR, c0 = (t % NTX) * TC;
     rs_fence_proxy_async();
+    if (MODE == 2) { rs_mbar_arrive_expect_tx(&bar[s], 0u); return; }
     rs_mbar_arrive_expect_tx(&bar[s], (unsigned)(SR * SW * 4));
     for (int b = 0; b < NB; ++b)  // NB boxes side by side: [SR][BW] each, stage layout [b][SR][BW]
-      rs_tma_load_2d(buf + s * STAGE + b * BS, &map, c0 - 4 + b * BW, r0 - 1, &bar[s]);
+      rs_tma_load_2d(buf + s * STAGE + b * BS, &map, c0 - PAD + b * BW, r0 - 1, &bar[s]);
   };
   if (tid == 0) {
     for (int q = 0; q < NSTAGE; ++q) rs_mbar_init(&bar[q], 1);
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(256) tilecopy(float* out, const __grid_constan
     float4 v[ROWS_PER];
 #pragma unroll
     for (int k = 0; k < ROWS_PER; ++k) {
-      const int e = tid + k * 256, y = e / CPR, x = (e % CPR) * 4 + 4;
+      const int e = tid + k * 256, y = e / CPR, x = (e % CPR) * 4 + PAD;
       const int b = x / BW, xb = x % BW;
       v[k] = *reinterpret_cast<const float4*>(tile + b * BS + (y + 1) * BW + xb);
     }
@@ -62,13 +63,15 @@ __global__ void __launch_bounds__(256) tilecopy(float* out, const __grid_constan
 #pragma unroll
     for (int k = 0; k < ROWS_PER; ++k) {
       const int e = tid + k * 256, y = e / CPR, x = (e % CPR) * 4;
-      *reinterpret_cast<float4*>(tile + y * TC + x) = v[k];
+      constexpr int OB = TC < 256 ? TC : 256;  // store boxes of <= 256 columns: staging [TC/OB][TR][OB]
+      *reinterpret_cast<float4*>(tile + (x / OB) * TR * OB + y * OB + x % OB) = v[k];
     }
     rs_fence_proxy_async();
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0 && MODE != 1) {
       const int r0 = (t / NTX) * TR, c0 = (t % NTX) * TC;
-      rs_tma_store_2d(&omap, c0, r0, tile);
+      constexpr int OB = TC < 256 ? TC : 256;
+      for (int b = 0; b < TC / OB; ++b) rs_tma_store_2d(&omap, c0 + b * OB, r0, tile + b * TR * OB);
       rs_bulk_commit();
     }
   }
@@ -85,24 +88,27 @@ def main():
     sets = [(torch.rand(H * W, device="cuda"), torch.empty(H * W, device="cuda")) for _ in range(2)]
     sm = torch.cuda.get_device_properties(0).multi_processor_count
     stream = torch.cuda.current_stream()
-    for (TR, TC, NB, NS, BPS) in [(64, 128, 1, 2, 3), (32, 128, 1, 2, 3), (32, 256, 2, 2, 3), (16, 512, 4, 2, 3), (64, 256, 2, 2, 2),
-                                  (128, 128, 1, 2, 2), (32, 256, 2, 3, 2), (64, 128, 1, 3, 2)]:
-        if TC % 4 or (TC + 8) % NB or ((TC + 8) // NB) > 256 or (TC + 8) // NB * 4 % 16:
+    cfgs = [(64, 128, 1, 2, 3, 4, 0), (64, 128, 1, 2, 3, 4, 1), (64, 128, 1, 2, 3, 4, 2),
+            (32, 256, 2, 2, 3, 4, 0), (32, 256, 2, 2, 3, 4, 1), (16, 512, 4, 2, 3, 8, 0),
+            (16, 512, 4, 3, 2, 8, 0), (16, 512, 4, 2, 3, 8, 1), (8, 1024, 8, 2, 3, 8, 0)]
+    for (TR, TC, NB, NS, BPS, PAD, MODE) in cfgs:
+        SW = TC + 2 * PAD
+        if SW % NB or SW // NB > 256 or (SW // NB) % 4:
             continue
         if W % TC or H % TR or (TR * TC // 4) % 256:
             continue
-        SR, SW = TR + 2, TC + 8
+        SR = TR + 2
         stage = NB * (-(-(SR * (SW // NB)) // 32) * 32)
         smem = NS * stage * 4 + 8 * NS + 128
         if smem * BPS > 227 * 1024:
             continue
-        name = f"tilecopy<{H}, {W}, {TR}, {TC}, {NB}, {NS}>"
+        name = f"tilecopy<{H}, {W}, {TR}, {TC}, {NB}, {NS}, {PAD}, {MODE}>"
         mod = rt.load_module(SRC, [name], ["--fmad=false"])
         fn = mod.function(mod.lowered[0])
         launches = []
         for src, dst in sets:
             m = rt.tma_desc_2d_f32(src.data_ptr(), W, H, W * 4, SW // NB, SR, 0)
-            om = rt.tma_desc_2d_f32(dst.data_ptr(), W, H, W * 4, TC, TR, 0)
+            om = rt.tma_desc_2d_f32(dst.data_ptr(), W, H, W * 4, min(TC, 256), TR, 0)
             ntiles = (W // TC) * (H // TR)
             grid = min(ntiles, sm * BPS)
             launches.append(rt.PreparedLaunch(fn, (grid, 1, 1), (256, 1, 1),
@@ -110,7 +116,7 @@ def main():
         for i in range(6):
             launches[i % 2]()
         torch.cuda.synchronize()
-        ok = torch.equal(sets[1][1], sets[1][0])
+        ok = torch.equal(sets[1][1], sets[1][0]) if MODE == 0 else None
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for i in range(40):
@@ -118,8 +124,9 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 40
-        print(f"TR={TR} TC={TC} boxes={NB} stages={NS} blocks/SM={BPS}: {ms * 1e3:.1f} us "
-              f"{2 * 4 * H * W / ms / 1e6:.0f} GB/s  exact={ok}", flush=True)
+        nbytes = (2 if MODE == 0 else 1) * 4 * H * W
+        print(f"TR={TR} TC={TC} boxes={NB} stages={NS} blocks/SM={BPS} mode={['copy', 'loads', 'stores'][MODE]}: "
+              f"{ms * 1e3:.1f} us {nbytes / ms / 1e6:.0f} GB/s  exact={ok}", flush=True)
 
 
 if __name__ == "__main__":

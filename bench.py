@@ -506,6 +506,13 @@ def run_ours(args, rank, world, local_rank):
     total_work = wl.work() if strong else wl.work() * world
     value = total_work / (ms * 1e-3) / 1e9
 
+    # SURVEY §8 e: the replicated operand / sharded result also measured with
+    # its collective inside the step (B all-gathered before the GEMM, y after
+    # the GEMV)
+    gathered = None
+    if world > 1 and wl.key in ("sgemm", "sgemm_nn", "gemv", "gemv_opt"):
+        gathered = _time_with_gather(wl, exe, dev_in, out, stream, dist, rank, world, args)
+
     # e2e: pinned host -> device, launch, device -> host, every step
     pinned = [torch.from_numpy(h.reshape(-1)).pin_memory() for h in host]
     host_out = torch.empty(exe.output_size, dtype=torch.float32).pin_memory()
@@ -578,6 +585,7 @@ def run_ours(args, rank, world, local_rank):
                                    "ms_per_step": round(e2e_seq_ms, 4),
                                    "path": "Executable.run_host: pinned H2D + launch + D2H on one stream"}},
             "gpu_launches": args.steps * n_stages,
+            **({"with_collective": gathered} if gathered else {}),
             "roofline": roof,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
@@ -666,6 +674,62 @@ def _bound_launch(exe, dev_in, out, stream, extra=None):
     buffers.update({spec["name"]: value for spec, value in zip(exe.plan["inputs"], dev_in)})
     buffers[exe.plan["output"]["name"]] = out
     return exe.bind(buffers, stream)
+
+
+def _time_with_gather(wl, exe, dev_in, out, stream, dist, rank, world, args):
+    """The multi-GPU step with its collective inside the timed region:
+    sgemm — every rank owns 1/G of the replicated operand's rows and the
+    step all-gathers it before the GEMM; gemv — the step all-gathers the
+    y blocks after the GEMV.  NCCL through the native runtime
+    (rs_allgather); gloo runs (CPU test path) stage through host tensors."""
+    import torch
+
+    native = dist.get_backend() == "nccl"
+    if wl.key.startswith("sgemm"):
+        recv = dev_in[1]
+        send = recv.view(world, -1)[rank].clone()
+        first, what = True, "the replicated operand all-gathered from 1/G row blocks before the GEMM, every step"
+    else:
+        send = out
+        recv = torch.empty(out.numel() * world, dtype=out.dtype, device=out.device)
+        first, what = False, "the y blocks all-gathered after the GEMV, every step"
+    launch = _bound_launch(exe, dev_in, out, stream)
+    comm = _device_comm() if native else None
+
+    def gather():
+        if native:
+            comm.allgather(send, recv, stream)
+            return
+        with torch.cuda.stream(stream):
+            parts = [torch.empty(send.numel(), dtype=send.dtype) for _ in range(world)]
+            dist.all_gather(parts, send.cpu())
+            recv.copy_(torch.cat(parts).to(recv.device))
+
+    def step():
+        if first:
+            gather()
+        launch()
+        if not first:
+            gather()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"value": round(wl.work() * world / (ms * 1e-3) / 1e9, 3), "unit": wl.metric_unit,
+            "ms_per_step": round(ms, 6), "collective": what,
+            "bytes_gathered_per_rank": int(recv.numel() * recv.element_size())}
 
 
 _COMM = []

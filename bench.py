@@ -257,7 +257,7 @@ class Nbody(Workload):
     key = "nbody"
     program = "all-pairs map/reduce + Euler velocity step (programs.NBODY)"
     config_index = 5
-    n = 131072
+    n = int(os.environ.get("RISE_NBODY_N", "131072"))  # (probes only; the config is 131072)
     metric_unit = "GFLOP/s"
     bound = "fp32-simt"
 

@@ -121,6 +121,11 @@ int rs_memcpy_htod(void* dst, const void* src, size_t bytes, void* stream);
 int rs_memcpy_dtoh(void* dst, const void* src, size_t bytes, void* stream);
 int rs_memcpy_dtod(void* dst, const void* src, size_t bytes, void* stream);
 int rs_memset_d8(void* dst, unsigned char value, size_t bytes, void* stream);
+/* Device-to-device copy between two GPUs of this node (cuMemcpyPeerAsync
+ * over NVLink / NVSwitch; SURVEY.md §8 b "rs_memcpy_...peer"): dst on
+ * dst_device, src on src_device, ordered on `stream` of the calling
+ * process's device.  src_device == dst_device is a plain device copy. */
+int rs_memcpy_peer(void* dst, int dst_device, const void* src, int src_device, size_t bytes, void* stream);
 
 /* ---- streams / events ------------------------------------------------ */
 

@@ -84,6 +84,7 @@ struct Driver {
   CUresult (*IpcOpenMemHandle)(CUdeviceptr*, CUipcMemHandle, unsigned);
   CUresult (*IpcCloseMemHandle)(CUdeviceptr);
   CUresult (*MemGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+  CUresult (*MemcpyPeerAsync)(CUdeviceptr, CUcontext, CUdeviceptr, CUcontext, size_t, CUstream);
 };
 
 Driver g_drv;
@@ -143,6 +144,7 @@ int load_driver() {
   ok &= sym(g_drv.IpcOpenMemHandle, "cuIpcOpenMemHandle_v2");
   ok &= sym(g_drv.IpcCloseMemHandle, "cuIpcCloseMemHandle");
   ok &= sym(g_drv.MemGetAddressRange, "cuMemGetAddressRange_v2");
+  ok &= sym(g_drv.MemcpyPeerAsync, "cuMemcpyPeerAsync");
   if (!ok) return fail("rs_init: the CUDA driver lacks a required entry point");
   g_drv.loaded = true;
   return 0;
@@ -483,6 +485,34 @@ int rs_memcpy_dtoh(void* dst, const void* src, size_t bytes, void* stream) {
 int rs_memcpy_dtod(void* dst, const void* src, size_t bytes, void* stream) {
   if (int e = ensure_ctx()) return e;
   CU(g_drv.MemcpyDtoDAsync((CUdeviceptr)dst, (CUdeviceptr)src, bytes, (CUstream)stream), "cuMemcpyDtoDAsync");
+  return 0;
+}
+
+// primary contexts of the other devices a peer copy names (retained once,
+// kept for the process: a copy may still be in flight when the call returns)
+CUcontext g_peer_ctx[64] = {};
+
+int rs_memcpy_peer(void* dst, int dst_device, const void* src, int src_device, size_t bytes, void* stream) {
+  if (int e = ensure_ctx()) return e;
+  int n = 0;
+  CU(g_drv.DeviceGetCount(&n), "cuDeviceGetCount");
+  if (dst_device < 0 || src_device < 0 || dst_device >= n || src_device >= n || n > 64)
+    return fail("rs_memcpy_peer: device %d -> %d out of range (%d devices)", src_device, dst_device, n);
+  CUcontext ctx[2] = {nullptr, nullptr};
+  const int devs[2] = {dst_device, src_device};
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    for (int i = 0; i < 2; ++i) {
+      if (!g_peer_ctx[devs[i]]) {
+        CUdevice d;
+        CU(g_drv.DeviceGet(&d, devs[i]), "cuDeviceGet");
+        CU(g_drv.DevicePrimaryCtxRetain(&g_peer_ctx[devs[i]], d), "cuDevicePrimaryCtxRetain");
+      }
+      ctx[i] = g_peer_ctx[devs[i]];
+    }
+  }
+  CU(g_drv.MemcpyPeerAsync((CUdeviceptr)dst, ctx[0], (CUdeviceptr)src, ctx[1], bytes, (CUstream)stream),
+     "cuMemcpyPeerAsync");
   return 0;
 }
 

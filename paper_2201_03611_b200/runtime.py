@@ -30,7 +30,7 @@ EXPORTED = (
     "rs_nvrtc_version", "rs_compile", "rs_compile_cubin", "rs_free_host", "rs_module_load",
     "rs_module_lowered_name", "rs_module_get_function", "rs_module_unload",
     "rs_function_attribute", "rs_launch", "rs_launch_ex", "rs_malloc", "rs_free", "rs_memcpy_htod",
-    "rs_memcpy_dtoh", "rs_memcpy_dtod", "rs_memset_d8", "rs_stream_create",
+    "rs_memcpy_dtoh", "rs_memcpy_dtod", "rs_memcpy_peer", "rs_memset_d8", "rs_stream_create",
     "rs_stream_destroy", "rs_stream_synchronize", "rs_device_synchronize", "rs_event_create",
     "rs_event_destroy", "rs_event_record", "rs_event_synchronize", "rs_event_elapsed_ms",
     "rs_tma_desc_2d_f32", "rs_ipc_handle", "rs_ipc_open", "rs_ipc_close", "rs_halo_exchange",
@@ -80,6 +80,7 @@ def lib():
             for name in ("rs_memcpy_htod", "rs_memcpy_dtoh", "rs_memcpy_dtod"):
                 getattr(L, name).argtypes = [vp, vp, sz, vp]
             L.rs_memset_d8.argtypes = [vp, ctypes.c_ubyte, sz, vp]
+            L.rs_memcpy_peer.argtypes = [vp, i, vp, i, sz, vp]
             L.rs_stream_create.argtypes = [ctypes.POINTER(vp)]
             L.rs_stream_destroy.argtypes = [vp]
             L.rs_stream_synchronize.argtypes = [vp]
@@ -324,6 +325,12 @@ def memcpy_htod(dst, src_host_ptr, nbytes, stream=None):
 
 def memcpy_dtoh(dst_host_ptr, src, nbytes, stream=None):
     check_run(lib().rs_memcpy_dtoh(_vp(dst_host_ptr), _vp(src), nbytes, _stream_ptr(stream)), "dtoh")
+
+
+def memcpy_peer(dst, dst_device, src, src_device, nbytes, stream=None):
+    """Device-to-device copy between two GPUs of the node (NVLink / NVSwitch)."""
+    check_run(lib().rs_memcpy_peer(_vp(dst), int(dst_device), _vp(src), int(src_device), nbytes,
+                                   _stream_ptr(stream)), "rs_memcpy_peer")
 
 
 def memset_d8(dst, value, nbytes, stream=None):

@@ -146,3 +146,17 @@ def test_cuda_graph_replays_a_multi_kernel_unit(gpu):
         g()
         stream.synchronize()
         np.testing.assert_array_equal(out.cpu().numpy(), want)
+
+
+def test_memcpy_peer_same_device(gpu):
+    # rs_memcpy_peer (cuMemcpyPeerAsync); on one GPU both ends are device 0
+    import torch
+
+    src = torch.arange(1 << 20, dtype=torch.float32, device="cuda")
+    dst = torch.zeros_like(src)
+    stream = torch.cuda.current_stream()
+    gpu.memcpy_peer(dst.data_ptr(), 0, src.data_ptr(), 0, src.numel() * 4, stream)
+    torch.cuda.synchronize()
+    assert torch.equal(dst, src)
+    with pytest.raises(Exception):
+        gpu.memcpy_peer(dst.data_ptr(), 0, src.data_ptr(), 99, 4, stream)

@@ -511,7 +511,10 @@ def run_ours(args, rank, world, local_rank):
     # the GEMV)
     gathered = None
     if world > 1 and wl.key in ("sgemm", "sgemm_nn", "gemv", "gemv_opt"):
-        gathered = _time_with_gather(wl, exe, dev_in, out, stream, dist, rank, world, args)
+        try:
+            gathered = _time_with_gather(wl, exe, dev_in, out, stream, dist, rank, world, args)
+        except Exception as exc:  # noqa: BLE001 - the headline line must still be printed
+            gathered = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
 
     # e2e: pinned host -> device, launch, device -> host, every step
     pinned = [torch.from_numpy(h.reshape(-1)).pin_memory() for h in host]

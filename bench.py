@@ -412,7 +412,13 @@ def run_ours(args, rank, world, local_rank):
             peer_sources = shard.PeerHaloRows(dev_in[0].view(nats["n"], nats["m"]), exe.plan["stages"][0]["halo_rows"])
             dist.barrier()
             extra.update(peer_sources.extra)
-        if exe.plan.get("peer_ranks"):
+        if any(st.get("peer_exchange") for st in exe.plan["stages"]):
+            from paper_2201_03611_b200 import shard
+
+            torch.cuda.synchronize()
+            peer_sources = shard.PeerExchange()
+            extra["rs_peer_table"] = peer_sources.table
+        elif exe.plan.get("peer_ranks"):
             from paper_2201_03611_b200 import shard
 
             torch.cuda.synchronize()
@@ -583,7 +589,9 @@ def run_ours(args, rank, world, local_rank):
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": round(e2e_ms, 4),
                     "path": ("Executable.stream_host: every step's pinned H2D, kernels and D2H, consecutive steps "
-                             "overlapped on three streams (double-buffered device sets)"),
+                             "overlapped on three streams (double-buffered device sets)" if peer_sources is None else
+                             "Executable.run_host (peer-memory kernels read or exchange through fixed buffers: "
+                             "one step at a time)"),
                     "sequential": {"value": round(total_work / (e2e_seq_ms * 1e-3) / 1e9, 3),
                                    "ms_per_step": round(e2e_seq_ms, 4),
                                    "path": "Executable.run_host: pinned H2D + launch + D2H on one stream"}},
@@ -611,7 +619,10 @@ def _parallelism_text(wl, world):
         "gemv_opt": f"weak: rank r owns an 8192-row band of an ({world}x8192) x 8192 matrix, x replicated",
         "sgemm": f"weak: rank r owns a 4096-row block of A ({world}x4096 rows), B replicated",
         "sgemm_nn": f"weak: rank r owns a 4096-row block of A ({world}x4096 rows), B replicated",
-        "dot": "weak: rank r owns a 2^24 chunk; partials all-gathered (rs_allgather, NCCL) and folded in rank order",
+        "dot": ("weak: rank r owns a 2^24 chunk; " + (
+            "the reduce kernel publishes its total into every rank's slots over NVLink (peer memory) and folds "
+            "the totals in rank order (exchange fused into the kernel)" if _dot_peer() else
+            "partials all-gathered (rs_allgather, NCCL) and folded in rank order")),
         "dot_chunked": "weak: rank r owns a 2^24 chunk; partials all-gathered (rs_allgather, NCCL), rank-order fold",
         "conv": ("weak: rank r owns an 8192-row band; " + (
             "the stencil kernel reads the neighbours' edge rows in place over NVLink (peer pointers, "
@@ -629,6 +640,11 @@ def _distributed_variant(wl, compiled, nats, host, rank, world):
     (paper_2201_03611_b200/shard.py)."""
     from paper_2201_03611_b200 import compile_program, programs
 
+    if wl.key == "dot" and _dot_peer():
+        # the fused variant: each rank's reduce kernel publishes its total into
+        # every rank's exchange slots (peer memory) and folds them in rank order
+        wl.emit_kwargs = {"peer_ranks": world}
+        return compiled, nats, host
     if wl.key == "conv" and _conv_fused_halo():
         # the fused variant: the stencil kernel reads its neighbours' edge rows
         # in place (peer pointers), so the band is exactly this rank's rows
@@ -663,6 +679,10 @@ def _distributed_variant(wl, compiled, nats, host, rank, world):
 
 def _nbody_peer():
     return os.environ.get("RISE_NBODY_PEER", "1") == "1"
+
+
+def _dot_peer():
+    return os.environ.get("RISE_DOT_PEER", "1") == "1"
 
 
 def _conv_fused_halo():

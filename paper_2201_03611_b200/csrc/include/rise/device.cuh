@@ -175,5 +175,25 @@ RS_DEVICE void rs_grid_sync(unsigned* bar) {
   __syncthreads();
 }
 
+// Cross-GPU exchange slot (peer memory, system scope): a 64-bit word
+// (epoch << 32 | payload bits).  rs_xchg_put publishes a value for `epoch`;
+// rs_xchg_get spins until the slot holds `epoch` and returns the payload.
+// A rank that never arrives traps after ~20 s instead of hanging the GPU.
+RS_DEVICE void rs_xchg_put(unsigned long long* slot, unsigned epoch, unsigned payload) {
+  const unsigned long long v = ((unsigned long long)epoch << 32) | payload;
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot), "l"(v) : "memory");
+}
+RS_DEVICE unsigned rs_xchg_get(const unsigned long long* slot, unsigned epoch) {
+  unsigned long long v, t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(slot) : "memory");
+    if ((unsigned)(v >> 32) == epoch) return (unsigned)v;
+    __nanosleep(100);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) __trap();  // a peer never published: fail loudly
+  }
+}
+
 RS_DEVICE unsigned rs_lane() { return threadIdx.x & 31u; }
 RS_DEVICE unsigned rs_warp() { return threadIdx.x >> 5; }

@@ -513,7 +513,8 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, pee
         entry = dict(generic.plan)
         match = idiom_mod.match(prog, st, base, temps, exact, reassociate) if idioms else None
         if peer_ranks and (match is None or not match.plan.get("peer_ranks")):
-            raise EmitError("peer_ranks needs a stage the allpairs template takes (sources read in place)")
+            raise EmitError("peer_ranks needs a stage the allpairs template (sources read in place) or the "
+                            "reduce template (totals exchanged in peer memory) takes")
         if peer_halo and (match is None or not match.plan.get("peer_halo")):
             raise EmitError("peer_halo needs a stage the stencil2d template takes (halo rows read in place)")
         if match is not None:

@@ -318,7 +318,13 @@ def _match_reduce(prog, stage, base_name, temps, exact):
     G = REDUCE_TMA_GRID if tma else REDUCE_GRID
     nthreads = B + 32 if tma else B
     minb = REDUCE_MINB
+    peers = int(getattr(prog, "peer_ranks", 0) or 0)
+    if peers and not (tma and ct == "float"):
+        return None
     xparams = [f"{ct}* __restrict__ rs_partials", "unsigned* __restrict__ rs_ticket"]
+    if peers:
+        # multi-GPU: the ranks' totals meet in peer memory (table: R slot arrays, then this rank)
+        xparams += ["const unsigned long long* __restrict__ rs_xtab", "unsigned* __restrict__ rs_epoch"]
     lines = kernel_head(prog, name, temps, launch_bounds=f"{nthreads}, {minb}", extra_params=xparams)
     lines += [
         f"  constexpr int RS_N4 = ({r(loop.bound)}) / 4;",
@@ -483,9 +489,28 @@ def _match_reduce(prog, stage, base_name, temps, exact):
         "    if (threadIdx.x == 0) {",
         "      // the n % 4 tail terms, in order, after the folded float4 part",
         f"      for (int rs_j = 4 * RS_N4; rs_j < {r(loop.bound)}; ++rs_j) rs_s = {add('rs_s', tail_term)};",
+    ]
+    if not peers:
+        lines += [
         f"      {ct} {acc.name} = {vr_plain(init.value)};",
         f"      {acc.name} = {add(acc.name, 'rs_s')};",
-    ]
+        ]
+    else:
+        lines += [
+            "      // this rank's total (its unit's own result), published to every rank's slot `me`;",
+            "      // then the R totals in rank order (every rank computes the same fold)",
+            f"      {ct} rs_mine = {vr_plain(init.value)};",
+            f"      rs_mine = {add('rs_mine', 'rs_s')};",
+            f"      constexpr int RS_R = {peers};",
+            "      const unsigned rs_e = ++*rs_epoch;  // this launch's epoch: every rank counts the same launches",
+            "      const int rs_me = (int)rs_xtab[RS_R];",
+            "      for (int rs_k = 0; rs_k < RS_R; ++rs_k)",
+            "        rs_xchg_put(reinterpret_cast<unsigned long long*>(rs_xtab[rs_k]) + rs_me, rs_e, __float_as_uint(rs_mine));",
+            "      const unsigned long long* rs_slots = reinterpret_cast<const unsigned long long*>(rs_xtab[rs_me]);",
+            f"      {ct} {acc.name} = __uint_as_float(rs_xchg_get(rs_slots, rs_e));",
+            "      for (int rs_k = 1; rs_k < RS_R; ++rs_k)",
+            f"        {acc.name} = {add(acc.name, '__uint_as_float(rs_xchg_get(rs_slots + rs_k, rs_e))')};",
+        ]
     for s_ in post:
         lines += [("      " + x) for x in thread_lines(prog, s_, exact)]
     lines += [
@@ -509,6 +534,12 @@ def _match_reduce(prog, stage, base_name, temps, exact):
                       {"name": ws_t, "ctype": "int", "size": "1"}],
         "extra_args": [{"kind": "workspace", "name": ws_p}, {"kind": "workspace", "name": ws_t}],
     }
+    if peers:
+        ws_e = f"rs_ws_{base_name}_epoch"
+        plan["workspace"].append({"name": ws_e, "ctype": "int", "size": "1"})
+        plan["extra_args"] += [{"kind": "peer_table"}, {"kind": "workspace", "name": ws_e}]
+        plan["peer_ranks"] = peers
+        plan["peer_exchange"] = True
     return IdiomKernel(name, "\n".join(lines) + "\n", plan)
 
 

@@ -216,6 +216,47 @@ class PeerSources:
         self.opened = []
 
 
+class PeerExchange:
+    """The exchange slots of a `reduce` kernel emitted with peer_ranks=R:
+    every rank owns R zeroed 64-bit slots (CUDA IPC-exported), maps everyone
+    else's, and hands the kernel a device table [slot array of rank 0 .. R-1,
+    this rank].  The kernel's last block writes this rank's total into slot
+    `rank` of every rank's array (a system-scope release store of
+    epoch << 32 | bits) and folds the R totals in rank order as they arrive
+    — the all-gather + rank-order sum of SURVEY.md §8 e C1 inside the
+    reduction kernel, no collective call."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import runtime
+
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.slots = torch.zeros(self.world, dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, runtime.ipc_handle(self.slots.data_ptr()), group=group)
+        self.opened = []
+        ptrs = []
+        for r in range(self.world):
+            if r == self.rank:
+                ptrs.append(int(self.slots.data_ptr()))
+            else:
+                p = runtime.ipc_open(*everyone[r])
+                self.opened.append(p)
+                ptrs.append(p)
+        self.table = torch.tensor(ptrs + [self.rank], dtype=torch.int64, device="cuda")
+        dist.barrier(group=group)
+
+    def close(self):
+        from . import runtime
+
+        for p in self.opened:
+            runtime.ipc_close(p)
+        self.opened = []
+
+
 class PeerHaloRows:
     """The halo rows of a `stencil2d` kernel emitted with peer_halo=True:
     each rank maps its neighbours' bands (CUDA IPC) once and hands the

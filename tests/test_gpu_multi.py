@@ -234,3 +234,60 @@ def test_halo_fused_into_the_stencil_bit_exact(world, n, m):
     for rank, ok, kinds in res:
         assert kinds == ["stencil2d"]
         assert ok, f"rank {rank}: fused-halo stencil differs from the oracle"
+
+
+def _dot_exchange_worker(rank, world, port, n, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2201_03611_b200 import emit_cuda, programs, shard
+        from paper_2201_03611_b200.run import Executable
+
+        torch.cuda.set_device(0)
+        c = programs.compile_config("dot")
+        a = torch.from_numpy(oracle.rng_inputs(30 + rank, n)).cuda()
+        b = torch.from_numpy(oracle.rng_inputs(40 + rank, n)).cuda()
+        # this rank's own total with the plain kernel, gathered and folded in rank order on the host
+        mine = Executable(emit_cuda(c.unit), {"n": n})(a, b).cpu()
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine)
+        want = parts[0].clone()
+        for p in parts[1:]:
+            want += p
+        # the fused kernel: totals exchanged in peer memory inside the reduction, several launches
+        code = emit_cuda(c.unit, peer_ranks=world)
+        ex = shard.PeerExchange()
+        exe = Executable(code, {"n": n})
+        outs = [exe(a, b, extra={"rs_peer_table": ex.table}).cpu() for _ in range(3)]
+        torch.cuda.synchronize()
+        dist.barrier()
+        ex.close()
+        same = all(np.array_equal(o.numpy().view(np.uint32), want.numpy().view(np.uint32)) for o in outs)
+        q.put((rank, same, exe.template_kinds))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 1 << 20), (3, (1 << 18) + 5)])
+def test_dot_totals_exchanged_in_peer_memory(world, n):
+    """C1's all-gather + rank-order sum fused into the reduce kernel: every
+    rank's last block publishes its total into every rank's slots (IPC peer
+    memory, epoch-tagged) and folds the totals in rank order — bit-identical
+    to gathering the per-rank totals and folding them on the host, launch
+    after launch.  (Two processes on one GPU time-slice, so each launch
+    waits for the other rank's kernel to run: slow here, not on N GPUs.)"""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dot_exchange_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, same, kinds in res:
+        assert kinds == ["reduce"]
+        assert same, f"rank {rank}: exchanged total differs from the rank-order fold"

@@ -45,18 +45,16 @@ def rows_per_block(nrows_py):
     """Rows per block as (Python expression of the sizes, C expression of
     RS_NROWS).
 
-    One lane folds one row, so a short, wide matrix (the chunked dot's 4096
-    chunks of 4096) leaves too few warps per SM to hide the shared-memory
-    latency of the fold; such shapes get 16 or 8 rows per block, i.e. at
-    least one block per SM (boxes of [R rows x 32 floats], same swizzle:
-    its pattern repeats every 8 rows)."""
+    One lane folds one row and a block is one warp, so the rows are dealt
+    out as evenly as the SMs allow: R = ceil(rows / (2 x 148)) clamped to
+    [8, 32] gives two blocks on (nearly) every SM.  8192 rows -> 28 rows
+    per block, 293 blocks (with 32 rows, 256 blocks leave 40 SMs one block
+    and 108 two: the two-block SMs set the time); 4096 rows -> 14."""
     if ROWS:
         return str(ROWS), str(ROWS)
-    # measured (B200): gemv 8192 rows 32 > 16 (0.864 / 0.849); chunked dot
-    # 4096 rows 16 = 32 > 8 — keep 32 until it leaves SMs without a block
-    t32, t16 = SM_COUNT * 32, SM_COUNT * 16
-    return (f"(32 if ({nrows_py}) > {t32} else (16 if ({nrows_py}) > {t16} else 8))",
-            f"(RS_NROWS > {t32} ? 32 : RS_NROWS > {t16} ? 16 : 8)")
+    slots = 2 * SM_COUNT
+    return (f"(32 if ({nrows_py}) > {32 * slots} else (8 if ({nrows_py}) <= {8 * slots} else -(-({nrows_py}) // {slots})))",
+            f"(RS_NROWS > {32 * slots} ? 32 : RS_NROWS <= {8 * slots} ? 8 : (RS_NROWS + {slots - 1}) / {slots})")
 
 
 def affine_in_flat_row(base, loops, assumptions):
@@ -120,16 +118,18 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
 
     nbox = KT // 32
     # stages stay 1024-byte aligned (128B swizzle)
-    stage_py = f"(-(-({len(rs_list) * nbox * 32} * {rows_py} + {len(sh_list) * KT}) // 256) * 256)"
+    boxrows_py = f"(-(-({rows_py}) // 8) * 8)"
+    stage_py = f"(-(-({len(rs_list) * nbox * 32} * {boxrows_py} + {len(sh_list) * KT}) // 256) * 256)"
     extra = [f"const __grid_constant__ rs_tmap rs_map{k}" for k in range(len(rs_list))]
     lines = kernel_head(prog, name, temps, launch_bounds=32, extra_params=extra)
     lines += [
         f"  constexpr int RS_NROWS = {r(nrows)};",
         f"  constexpr int RS_ROWS = {rows_c}, RS_KT = {KT}, RS_STAGES = {STAGES}, RS_NBOX = {nbox};",
         "  constexpr unsigned RS_MASK = RS_ROWS == 32 ? 0xffffffffu : (1u << RS_ROWS) - 1u;",
+        "  constexpr int RS_BR = (RS_ROWS + 7) / 8 * 8;  // a box's rows in shared memory (1024-byte swizzle atoms)",
         f"  constexpr int RS_K = {r(loop.bound)};",
         "  constexpr int RS_NT = (RS_K + RS_KT - 1) / RS_KT;",
-        f"  constexpr int RS_STAGE_FLOATS = ({len(rs_list) * nbox * 32} * RS_ROWS + {len(sh_list) * KT} + 255) / 256 * 256;",
+        f"  constexpr int RS_STAGE_FLOATS = ({len(rs_list) * nbox * 32} * RS_BR + {len(sh_list) * KT} + 255) / 256 * 256;",
         "  extern __shared__ __align__(1024) unsigned char rs_smem_raw[];",
         "  float* rs_smem = reinterpret_cast<float*>(rs_smem_raw + ((1024u - (rs_smem_addr(rs_smem_raw) & 1023u)) & 1023u));",
         "  unsigned long long* rs_bar = reinterpret_cast<unsigned long long*>(rs_smem + RS_STAGES * RS_STAGE_FLOATS);",
@@ -178,11 +178,11 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
     for k in range(len(rs_list)):
         lines += [
             "      for (int rs_b = 0; rs_b < rs_nb; ++rs_b)",
-            f"        rs_tma_load_2d(rs_st + ({k} * RS_NBOX + rs_b) * 32 * RS_ROWS, &rs_map{k}, rs_j0 + 32 * rs_b, rs_row0,"
+            f"        rs_tma_load_2d(rs_st + ({k} * RS_NBOX + rs_b) * 32 * RS_BR, &rs_map{k}, rs_j0 + 32 * rs_b, rs_row0,"
             " &rs_bar[rs_slot]);",
         ]
     for k in range(len(sh_list)):
-        off = f"{len(rs_list)} * RS_NBOX * 32 * RS_ROWS + {k} * RS_KT"
+        off = f"{len(rs_list)} * RS_NBOX * 32 * RS_BR + {k} * RS_KT"
         lines.append(f"      rs_bulk_g2s(rs_st + {off}, rs_gx{k} + rs_j0, (unsigned)rs_kt * 4u, &rs_bar[rs_slot]);")
     lines += [
         "    }",
@@ -211,10 +211,10 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
         ]
         for k in range(len(rs_list)):
             out.append(
-                f"{p}const float4 rs_a{k} = *reinterpret_cast<const float4*>(rs_st + ({k} * RS_NBOX + rs_box) * 32 * RS_ROWS"
+                f"{p}const float4 rs_a{k} = *reinterpret_cast<const float4*>(rs_st + ({k} * RS_NBOX + rs_box) * 32 * RS_BR"
                 f" + rs_lane * 32 + rs_chunk * 4);")
         for k in range(len(sh_list)):
-            off = f"{len(rs_list)} * RS_NBOX * 32 * RS_ROWS + {k} * RS_KT"
+            off = f"{len(rs_list)} * RS_NBOX * 32 * RS_BR + {k} * RS_KT"
             out.append(f"{p}const float4 rs_x{k} = *reinterpret_cast<const float4*>(rs_st + {off} + rs_jj);")
         for comp in ("x", "y", "z", "w"):
             out.append(f"{p}{acc.name} = {step_with(comp)};")

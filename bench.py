@@ -703,8 +703,9 @@ def _time_with_gather(wl, exe, dev_in, out, stream, dist, rank, world, args):
     """The multi-GPU step with its collective inside the timed region:
     sgemm — every rank owns 1/G of the replicated operand's rows and the
     step all-gathers it before the GEMM; gemv — the step all-gathers the
-    y blocks after the GEMV.  NCCL through the native runtime
-    (rs_allgather); gloo runs (CPU test path) stage through host tensors."""
+    y blocks after the GEMV.  NCCL (the process group's communicator, or the
+    runtime's rs_allgather with RISE_GATHER_NATIVE=1); gloo runs (CPU test
+    path) stage through host tensors."""
     import torch
 
     native = dist.get_backend() == "nccl"
@@ -717,11 +718,17 @@ def _time_with_gather(wl, exe, dev_in, out, stream, dist, rank, world, args):
         recv = torch.empty(out.numel() * world, dtype=out.dtype, device=out.device)
         first, what = False, "the y blocks all-gathered after the GEMV, every step"
     launch = _bound_launch(exe, dev_in, out, stream)
-    comm = _device_comm() if native else None
+    # the process group's own NCCL communicator (no second communicator for a
+    # reporting variant; RISE_GATHER_NATIVE=1 uses the runtime's rs_allgather)
+    comm = _device_comm() if native and os.environ.get("RISE_GATHER_NATIVE", "0") == "1" else None
 
     def gather():
-        if native:
+        if comm is not None:
             comm.allgather(send, recv, stream)
+            return
+        if native:
+            with torch.cuda.stream(stream):
+                dist.all_gather_into_tensor(recv, send)
             return
         with torch.cuda.stream(stream):
             parts = [torch.empty(send.numel(), dtype=send.dtype) for _ in range(world)]

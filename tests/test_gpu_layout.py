@@ -120,3 +120,15 @@ def test_conv5_stencil_template_bit_exact(gpu, n, m):
             acc = (acc + (p[i:i + n, j:j + m] * w[i, j]).astype(np.float32)).astype(np.float32)
         total = (total + acc).astype(np.float32)
     np.testing.assert_array_equal(got.reshape(n, m), total)
+
+
+@pytest.mark.parametrize("n,m", [(300, 516), (128, 128), (1000, 8), (4, 2052), (8192, 8192)])
+def test_transpose_template_bit_exact(gpu, n, m):
+    # the transpose2d template (TMA-swizzled 128 x 128 tiles); pitch % 4 == 0 sizes take it
+    rng = np.random.default_rng(n + m)
+    M = rng.standard_normal((n, m)).astype(np.float32)
+    c = compile_program(PROGRAMS["transposeCopy"][0], None, name="transposeCopy")
+    code = emit_cuda(c.unit)
+    assert code.plan["stages"][0]["kind"] == "transpose2d"
+    got = run_cuda(code, c.unit, {"n": n, "m": m}, [M], as_numpy=True)
+    np.testing.assert_array_equal(got.reshape(m, n), M.T)

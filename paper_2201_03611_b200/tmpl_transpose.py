@@ -36,8 +36,6 @@ BLOCK = 256
 def _affine2(index, rv, cv, params):
     """index = base + a * rv + b * cv with base, a, b free of rv / cv (sizes
     only): (base, a, b), else None."""
-    z = {rv: nat.Const(0), cv: nat.Const(0)}
-
     def at(r, c):
         return nat.normalize(nat.substitute(index, {rv: nat.Const(r), cv: nat.Const(c)}))
 
@@ -52,7 +50,6 @@ def _affine2(index, rv, cv, params):
     for e in (base, a, b):
         if not nat.free_vars(e) <= set(params):
             return None
-    del z
     return base, a, b
 
 
@@ -92,7 +89,8 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     pre = [f"({py_expr(R)}) > 0", f"({py_expr(C)}) > 0"]
     tmaps = []
     for buf, base, pitch in s_list:
-        pre += [f"({py_expr(base)}) % 4 == 0", f"({py_expr(pitch)}) % 4 == 0", f"({py_expr(pitch)}) > 0"]
+        # (16-byte aligned base and pitch; rows of the read region must not overlap: R <= P)
+        pre += [f"({py_expr(base)}) % 4 == 0", f"({py_expr(pitch)}) % 4 == 0", f"({py_expr(pitch)}) >= ({py_expr(R)})"]
         tmaps.append({"kind": "tma2d", "buf": buf, "offset": py_expr(base), "dims": [py_expr(R), py_expr(C)],
                       "pitch": py_expr(pitch), "box": [BOX, T], "swizzle": 3})
     pre = list(dict.fromkeys(pre))

@@ -23,7 +23,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
-from . import lir, tmpl_allpairs, tmpl_gemm, tmpl_iterate, tmpl_rowfold, tmpl_seqfold, tmpl_stencil, tmpl_transpose
+from . import lir, tmpl_allpairs, tmpl_gemm, tmpl_iterate, tmpl_rowfold, tmpl_seqfold, tmpl_stencil, tmpl_stencil1d, tmpl_transpose
 from ._ref import nat
 from .emit_cuda import NatRenderer, ValueRenderer, collapse_global_chain, kernel_head, py_expr
 
@@ -36,7 +36,8 @@ class IdiomKernel:
     includes: list = field(default_factory=list)
 
 
-ORDER_PRESERVING = ("_match_rowfold", "_match_stencil", "_match_seqfold", "_match_iterate", "_match_transpose")
+ORDER_PRESERVING = ("_match_rowfold", "_match_stencil", "_match_seqfold", "_match_iterate", "_match_transpose",
+                    "_match_stencil1d")
 
 
 def _match_iterate(prog, stage, base_name, temps, exact):
@@ -57,7 +58,7 @@ def _match_seqfold(prog, stage, base_name, temps, exact):
 
 def match(prog, stage, base_name, temps, exact, reassociate=True):
     for matcher in (_match_gemm, _match_rowfold, _match_reduce, _match_stencil, _match_allpairs,
-                    _match_seqfold, _match_iterate, _match_transpose):
+                    _match_seqfold, _match_iterate, _match_transpose, _match_stencil1d):
         if not reassociate and matcher.__name__ not in ORDER_PRESERVING:
             continue
         out = matcher(prog, stage, base_name, temps, exact)
@@ -76,6 +77,14 @@ def _match_gemm(prog, stage, base_name, temps, exact):
 
 def _match_allpairs(prog, stage, base_name, temps, exact):
     out = tmpl_allpairs.match(prog, stage, base_name, temps, exact, parallel_rows)
+    if out is None:
+        return None
+    text, plan = out
+    return IdiomKernel(plan["name"], text, plan)
+
+
+def _match_stencil1d(prog, stage, base_name, temps, exact):
+    out = tmpl_stencil1d.match(prog, stage, base_name, temps, exact, parallel_rows)
     if out is None:
         return None
     text, plan = out
@@ -564,4 +573,5 @@ LAUNCHERS = {
     "seqfold": tmpl_seqfold.launch,
     "iterate": tmpl_iterate.launch,
     "transpose2d": tmpl_transpose.launch,
+    "stencil1d": tmpl_stencil1d.launch,
 }

@@ -132,3 +132,30 @@ def test_transpose_template_bit_exact(gpu, n, m):
     assert code.plan["stages"][0]["kind"] == "transpose2d"
     got = run_cuda(code, c.unit, {"n": n, "m": m}, [M], as_numpy=True)
     np.testing.assert_array_equal(got.reshape(m, n), M.T)
+
+
+SLIDE5 = ("depFun((n: Nat) => fun(xs: Array[n, f32] => xs |> padClamp(2)(2) |> slide(5)(1) "
+          "|> mapGlobal(fun(w => w |> reduceSeq(Private)(fun(a, v => a + v * 0.5f))(0.0f)))))")
+
+
+@pytest.mark.parametrize("n", [4, 8, 4096, 4100, 8192 + 12, 1 << 20])
+def test_stencil1d_template_bit_exact(gpu, n):
+    # the stencil1d template (one bulk copy per 4096-output tile, padClamp in shared memory)
+    rng = np.random.default_rng(n)
+    xs = rng.standard_normal(n).astype(np.float32)
+    c = compile_program(PROGRAMS["slide1D"][0], None, name="slide1D")
+    code = emit_cuda(c.unit)
+    assert code.plan["stages"][0]["kind"] == "stencil1d"
+    got = run_cuda(code, c.unit, {"n": n}, [xs], as_numpy=True)
+    p = np.pad(xs, (1, 1), mode="edge")
+    want = ((np.float32(0) + p[:-2]) + p[1:-1]) + p[2:]
+    np.testing.assert_array_equal(got, want.astype(np.float32))
+    c5 = compile_program(SLIDE5, None, name="slide5")
+    code5 = emit_cuda(c5.unit)
+    assert code5.plan["stages"][0]["kind"] == "stencil1d"
+    got5 = run_cuda(code5, c5.unit, {"n": n}, [xs], as_numpy=True)
+    p5 = np.pad(xs, (2, 2), mode="edge")
+    acc = np.zeros(n, np.float32)
+    for k in range(5):
+        acc = (acc + p5[k:k + n] * np.float32(0.5)).astype(np.float32)
+    np.testing.assert_array_equal(got5, acc)

@@ -185,3 +185,16 @@ def test_split_reduce_refuses_unknown_identities():
     from paper_2201_03611_b200._ref import rules
 
     assert any(r.startswith("splitReduce(") for r in rules.describe_rules())
+
+
+def test_stencil_persistent_grid_avoids_power_of_two_tile_strides():
+    # the tile stride of the persistent stencil blocks is kept at 2 (mod 4):
+    # multiples of the strips per band pile every block onto one column strip
+    # (and the same HBM channels) — DESIGN.md §3 stencil2d
+    from paper_2201_03611_b200 import programs, tmpl_stencil
+
+    c = programs.compile_config("conv")
+    st = emit_cuda(c.unit).plan["stages"][0]
+    for n, m in [(8192, 8192), (4096, 8192), (8192, 16384)]:
+        (grid, _, _), block, smem, _ = tmpl_stencil.launch(st, {"n": n, "m": m}, 148)
+        assert grid % 4 == 2 and grid <= 148 * st["blocks_per_sm"]

@@ -37,7 +37,9 @@ import os  # noqa: E402
 ROWS = int(os.environ.get("RISE_ROWFOLD_ROWS", "0"))  # rows per block (8, 16 or 32); 0 = by row count
 
 KT = int(os.environ.get("RISE_ROWFOLD_KT", "256"))  # columns per stage (KT/32 TMA boxes of 32 columns)
-STAGES = int(os.environ.get("RISE_ROWFOLD_STAGES", "2"))  # measured (gemv 8192²): 128x6 0.835, 256x2 0.855, 512x2 0.65
+# measured (gemv 8192², L2 flushed, 32-row blocks): 128x6 0.835, 256x2 0.855, 512x2 0.65; (round-robin
+# inputs, 28-row blocks, two passes): 256x2 0.924-0.929, 256x3 0.936-0.939 (chunked dot 0.563 -> 0.583)
+STAGES = int(os.environ.get("RISE_ROWFOLD_STAGES", "3"))
 SM_COUNT = 148
 
 

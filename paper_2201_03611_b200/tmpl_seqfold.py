@@ -19,11 +19,13 @@ the next 16 elements while the current 16 are folded).  Order: PRESERVED (bit-ex
 
 from __future__ import annotations
 
+import os
+
 from . import lir
 from ._ref import nat
 from .emit_cuda import NatRenderer, ValueRenderer, kernel_head, py_expr
 
-TILE = 2048  # floats per stage (split among the streams: static smem stays < 48 KB)
+TILE = int(os.environ.get("RISE_SEQFOLD_TILE", "2048"))  # floats per stage (split among the streams: static smem < 48 KB)
 STAGES = 3
 
 

@@ -198,3 +198,22 @@ def test_stencil_persistent_grid_avoids_power_of_two_tile_strides():
     for n, m in [(8192, 8192), (4096, 8192), (8192, 16384)]:
         (grid, _, _), block, smem, _ = tmpl_stencil.launch(st, {"n": n, "m": m}, 148)
         assert grid % 4 == 2 and grid <= 148 * st["blocks_per_sm"]
+
+
+@pytest.mark.parametrize("name,source,nats,kind", [
+    ("transposeCopy", "depFun((n: Nat, m: Nat) => fun(M: Array[n, Array[m, f32]] => "
+     "M |> transpose |> mapGlobal(mapGlobal(fun(v => v * 1.0f)))))", {"n": 8192, "m": 8192}, "transpose2d"),
+    ("slide1D", "depFun((n: Nat) => fun(xs: Array[n, f32] => xs |> padClamp(1)(1) |> slide(3)(1) "
+     "|> mapGlobal(fun(w => w |> reduceSeq(Private)(fun(a, v => a + v))(0.0f)))))", {"n": 1 << 26}, "stencil1d"),
+])
+def test_layout_templates_selected_and_compile(name, source, nats, kind):
+    """The layout templates (transpose2d, stencil1d) take their programs,
+    keep the program's order (also under reassociate=False) and compile."""
+    c = compile_program(source, None, name=name)
+    for reassociate in (True, False):
+        code = emit_cuda(c.unit, reassociate=reassociate)
+        assert [s["kind"] for s in code.plan["stages"]] == [kind]
+    targs = ", ".join(str(nats[p]) for p in code.plan["nat_params"])
+    names = [f"{s['name']}<{targs}>" for st in code.plan["stages"] for s in (st, st.get("fallback")) if s]
+    cubin, lowered = runtime.compile_cubin(code.text, names, ["--fmad=false"])
+    assert cubin[:4] == b"\x7fELF" and len(lowered) == len(names)

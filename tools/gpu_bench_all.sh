@@ -9,5 +9,6 @@ for w in ${WORKLOADS:-gemv gemv_opt dot dot_chunked conv sgemm sgemm_nn nbody}; 
   timeout 600 python bench.py --impl reference --workload $w --steps 3 --warmup 3 > gpurun_out/bench/ref_$w.json 2> gpurun_out/bench/ref_$w.err
 done
 timeout 600 python bench.py > gpurun_out/bench/bench_default.json 2> gpurun_out/bench/bench_default.err
+timeout 300 python tools/probe_transpose.py > gpurun_out/bench/layout_programs.txt 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bench/launches_gemv.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 echo done

@@ -570,7 +570,7 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
 // 2..5 hi/lo converters, 6..9 epilogue (TMEM lane quarter = warp % 4).
 constexpr int PTHREADS = 320;
 
-template <int M, int N, int K, int BN, int STAGES, bool B_MN = false>
+template <int M, int N, int K, int BN, int STAGES, bool B_MN = false, int GROUP_M = 0>
 RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const rs_tmap* mapA, const rs_tmap* mapB,
                                           int n_full, int n_units, float* __restrict__ ws,
                                           unsigned* __restrict__ flags) {
@@ -604,8 +604,16 @@ RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const 
     khalf = split ? (sidx & 1) : 0;
     kb0 = split && khalf ? KB / 2 : 0;
     kb1 = split && !khalf ? KB / 2 : KB;
-    m0 = (tile / NTN) * 256;
-    n0 = (tile % NTN) * BN;
+    if (GROUP_M > 0) {  // tiles in groups of GROUP_M row tiles, column by column (L2 reuse of A and B)
+      constexpr int NTM = (M + 255) / 256;
+      const int grp = tile / (GROUP_M * NTN), r = tile % (GROUP_M * NTN);
+      const int rows = NTM - grp * GROUP_M < GROUP_M ? NTM - grp * GROUP_M : GROUP_M;
+      m0 = (grp * GROUP_M + r % rows) * 256;
+      n0 = (r / rows) * BN;
+    } else {
+      m0 = (tile / NTN) * 256;
+      n0 = (tile % NTN) * BN;
+    }
   };
 
   if (threadIdx.x == 0) {

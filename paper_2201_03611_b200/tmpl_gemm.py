@@ -34,6 +34,7 @@ PAIR_BN = int(os.environ.get("RISE_GEMM_PAIR_BN", "256"))
 PAIR_STAGES = int(os.environ.get("RISE_GEMM_PAIR_STAGES", "3"))
 # persistent CTA pairs with a double-buffered TMEM accumulator and dedicated
 # epilogue warps (gemm_3xtf32_2sm_persistent)
+GROUP_M = int(os.environ.get("RISE_GEMM_GROUP_M", "8"))  # persistent tile order: groups of 8 row tiles, column by column (measured +0.6 %; 0 = row-major)
 PERSIST = os.environ.get("RISE_GEMM_PERSIST", "1") == "1"  # measured 278 -> 284 TFLOP/s
 
 
@@ -98,7 +99,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
         args = "rs_nfull, rs_nunits, rs_ws, rs_flags" if PERSIST else "rs_nfull, rs_ws, rs_flags"
         lines += [
             f"  rise_gemm::{fn}<{r(M)}, {r(N)}, {r(K)}, {PAIR_BN}, {PAIR_STAGES}, "
-            f"{'true' if b_mn else 'false'}>"
+            f"{'true' if b_mn else 'false'}{(', ' + str(GROUP_M)) if PERSIST and GROUP_M else ''}>"
             f"({st.target.buf}, {r(N)}, &rs_mapA, &rs_mapB, {args});",
             "}",
         ]

@@ -122,16 +122,23 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
     # stages stay 1024-byte aligned (128B swizzle)
     boxrows_py = f"(-(-({rows_py}) // 8) * 8)"
     stage_py = f"(-(-({len(rs_list) * nbox * 32} * {boxrows_py} + {len(sh_list) * KT}) // 256) * 256)"
+    # ring depth: up to STAGES, as many as fit two blocks per SM for the block's rows
+    # (at least one: a one-stage ring issues each stage just before it waits on it)
+    budget = 113 * 1024
+    stages_py = (f"({STAGES} if {budget} // ({stage_py} * 4) >= {STAGES} else "
+                 f"(1 if {budget} // ({stage_py} * 4) < 1 else {budget} // ({stage_py} * 4)))")
     extra = [f"const __grid_constant__ rs_tmap rs_map{k}" for k in range(len(rs_list))]
     lines = kernel_head(prog, name, temps, launch_bounds=32, extra_params=extra)
     lines += [
         f"  constexpr int RS_NROWS = {r(nrows)};",
-        f"  constexpr int RS_ROWS = {rows_c}, RS_KT = {KT}, RS_STAGES = {STAGES}, RS_NBOX = {nbox};",
+        f"  constexpr int RS_ROWS = {rows_c}, RS_KT = {KT}, RS_NBOX = {nbox};",
         "  constexpr unsigned RS_MASK = RS_ROWS == 32 ? 0xffffffffu : (1u << RS_ROWS) - 1u;",
         "  constexpr int RS_BR = (RS_ROWS + 7) / 8 * 8;  // a box's rows in shared memory (1024-byte swizzle atoms)",
         f"  constexpr int RS_K = {r(loop.bound)};",
         "  constexpr int RS_NT = (RS_K + RS_KT - 1) / RS_KT;",
         f"  constexpr int RS_STAGE_FLOATS = ({len(rs_list) * nbox * 32} * RS_BR + {len(sh_list) * KT} + 255) / 256 * 256;",
+        f"  constexpr int RS_FIT = {budget} / (RS_STAGE_FLOATS * 4);  // stages two blocks per SM can hold",
+        f"  constexpr int RS_STAGES = RS_FIT >= {STAGES} ? {STAGES} : (RS_FIT < 1 ? 1 : RS_FIT);",
         "  extern __shared__ __align__(1024) unsigned char rs_smem_raw[];",
         "  float* rs_smem = reinterpret_cast<float*>(rs_smem_raw + ((1024u - (rs_smem_addr(rs_smem_raw) & 1023u)) & 1023u));",
         "  unsigned long long* rs_bar = reinterpret_cast<unsigned long long*>(rs_smem + RS_STAGES * RS_STAGE_FLOATS);",
@@ -253,7 +260,7 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
         g = GenericKernel(prog, Stage("serial", s), "_", [], exact)
         lines += [("    " + x) for x in g.thread(s, 0)]
     lines += ["  }", "}"]
-    smem = f"{STAGES} * {stage_py} * 4 + {STAGES * 8 + 1024}"
+    smem = f"{stages_py} * {stage_py} * 4 + {stages_py} * 8 + 1024"
     plan = {
         "name": name,
         "kind": "rowfold",

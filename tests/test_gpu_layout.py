@@ -159,3 +159,24 @@ def test_stencil1d_template_bit_exact(gpu, n):
     for k in range(5):
         acc = (acc + p5[k:k + n] * np.float32(0.5)).astype(np.float32)
     np.testing.assert_array_equal(got5, acc)
+
+
+ROW3 = ("depFun((n: Nat, m: Nat) => fun(A: Array[n, Array[m, f32]] => fun(B: Array[n, Array[m, f32]] => "
+        "fun(C: Array[n, Array[m, f32]] => zip(A)(zip(B)(C)) |> mapGlobal(fun(r => "
+        "zip(fst(r))(zip(fst(snd(r)))(snd(snd(r)))) |> reduceSeq(Private)(fun(acc, t => "
+        "acc + fst(t) * fst(snd(t)) * snd(snd(t))))(0.0f)))))))")
+
+
+@pytest.mark.parametrize("n,m", [(8192, 512), (1000, 1028)])
+def test_rowfold_three_row_streams_bit_exact(gpu, n, m):
+    # three row streams: the ring depth shrinks to what fits two blocks per SM
+    rng = np.random.default_rng(n)
+    A, B, C = (rng.standard_normal((n, m)).astype(np.float32) for _ in range(3))
+    c = compile_program(ROW3, None, name="row3")
+    code = emit_cuda(c.unit)
+    assert code.plan["stages"][0]["kind"] == "rowfold"
+    got = run_cuda(code, c.unit, {"n": n, "m": m}, [A, B, C], as_numpy=True)
+    acc = np.zeros(n, np.float32)
+    for j in range(m):
+        acc = (acc + (A[:, j] * B[:, j]) * C[:, j]).astype(np.float32)
+    np.testing.assert_array_equal(got, acc)

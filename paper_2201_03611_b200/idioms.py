@@ -356,7 +356,10 @@ def _match_reduce(prog, stage, base_name, temps, exact):
     if tma:
         NSTR = len(s_list)
         CH4 = REDUCE_TMA_CHUNK // 16
-        S = REDUCE_TMA_STAGES
+        # ring depth within ~200 KiB of shared memory (many input streams: fewer stages)
+        S = min(REDUCE_TMA_STAGES, (200 * 1024) // (NSTR * CH4 * 16))
+        if S < 2:
+            return None  # too many streams for a double-buffered ring: the generic kernel
         smem = S * NSTR * CH4 * 16 + 2 * S * 8
         lines += [
             f"  constexpr int RS_CH4 = {CH4}, RS_S = {S}, RS_NSTR = {NSTR};",

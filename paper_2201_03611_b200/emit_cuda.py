@@ -38,6 +38,7 @@ from __future__ import annotations
 
 import json
 import os
+import warnings
 from dataclasses import dataclass, field
 
 from . import lir
@@ -479,6 +480,10 @@ def arg_names(prog: lir.Program, temps):
 # whole units
 
 
+class SingleBlockStage(UserWarning):
+    """A kernel stage that runs in one block / one thread on the GPU."""
+
+
 def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, peer_halo=False) -> CudaCode:
     """Emit the sm100a kernel text (and launch plan) for an ImperativeUnit.
 
@@ -523,6 +528,12 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, pee
                 if inc not in includes:
                     includes.append(inc)
             entry = dict(match.plan, fallback=generic.plan)
+        elif st.kind in ("block", "serial"):
+            # a top-level sequential loop (or fold) no template claims runs in ONE
+            # block (one thread for "serial"): correct, but a performance cliff
+            entry["single_block"] = True
+            warnings.warn(f"{base}: stage {st.index} runs as a single-{'block' if st.kind == 'block' else 'thread'} "
+                          "kernel (a top-level sequential loop no template claims)", SingleBlockStage, stacklevel=2)
         plan_stages.append(entry)
     if PDL and len(stages) > 1:
         # programmatic dependent launch: stage k > 0 may be scheduled while

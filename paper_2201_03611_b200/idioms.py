@@ -254,12 +254,19 @@ REDUCE_TMA_CONTIG = os.environ.get("RISE_REDUCE_TMA_CONTIG", "0") == "1"
 REDUCE_EARLY = os.environ.get("RISE_REDUCE_EARLY", "1") == "1"  # 2-D tensor-map boxes instead of bulk copies
 
 
-def reduce_fold_length(n: int) -> int:
+def _reduce_tma_stages(nstreams: int) -> int:
+    """Ring depth of the TMA variant for `nstreams` input streams (~200 KiB of
+    shared memory); < 2 means the register-batched LDG variant is emitted."""
+    return min(REDUCE_TMA_STAGES, (200 * 1024) // (nstreams * REDUCE_TMA_CHUNK))
+
+
+def reduce_fold_length(n: int, streams: int = 2) -> int:
     """Terms one thread folds sequentially in phase 1 of the `reduce`
-    template for n terms (its error bound's sequential part)."""
+    template for n terms read from `streams` input streams (its error
+    bound's sequential part)."""
     n4 = n // 4
     tail = n - 4 * n4  # folded after the float4 part by the last block
-    if REDUCE_TMA:
+    if REDUCE_TMA and _reduce_tma_stages(streams) >= 2:
         ch4 = REDUCE_TMA_CHUNK // 16
         chunks = -(-n4 // ch4)
         return 4 * -(-chunks // REDUCE_TMA_GRID) * -(-ch4 // REDUCE_BLOCK) + tail
@@ -332,7 +339,10 @@ def _match_reduce(prog, stage, base_name, temps, exact):
     tail_term = ValueRenderer(prog, exact, load_hook=tail_hook)(term)
     shfl = "__shfl_xor_sync(0xffffffffu, rs_s, rs_o)"
     U = REDUCE_BATCH
-    tma = REDUCE_TMA
+    s_list = list(dict.fromkeys(streams.values()))
+    # many input streams: when not even a double-buffered TMA ring fits, the
+    # register-batched LDG variant (any number of streams) is emitted instead
+    tma = REDUCE_TMA and _reduce_tma_stages(len(s_list)) >= 2
     B = REDUCE_BLOCK  # threads that fold (the TMA variant adds one producer warp)
     G = REDUCE_TMA_GRID if tma else REDUCE_GRID
     nthreads = B + 32 if tma else B
@@ -357,9 +367,7 @@ def _match_reduce(prog, stage, base_name, temps, exact):
         NSTR = len(s_list)
         CH4 = REDUCE_TMA_CHUNK // 16
         # ring depth within ~200 KiB of shared memory (many input streams: fewer stages)
-        S = min(REDUCE_TMA_STAGES, (200 * 1024) // (NSTR * CH4 * 16))
-        if S < 2:
-            return None  # too many streams for a double-buffered ring: the generic kernel
+        S = _reduce_tma_stages(NSTR)
         smem = S * NSTR * CH4 * 16 + 2 * S * 8
         lines += [
             f"  constexpr int RS_CH4 = {CH4}, RS_S = {S}, RS_NSTR = {NSTR};",
@@ -526,9 +534,14 @@ def _match_reduce(prog, stage, base_name, temps, exact):
             f"      constexpr int RS_R = {peers};",
             "      const unsigned rs_e = ++*rs_epoch;  // this launch's epoch: every rank counts the same launches",
             "      const int rs_me = (int)rs_xtab[RS_R];",
+            "      // two slot banks by epoch parity: a rank that has read every epoch-e total may publish",
+            "      // e + 1 before a slower rank has read e; it cannot reach e + 2 before that rank",
+            "      // has published e + 1, i.e. finished reading e — so no slot is overwritten unread",
+            "      const int rs_bank = (int)(rs_e & 1u) * RS_R;",
             "      for (int rs_k = 0; rs_k < RS_R; ++rs_k)",
-            "        rs_xchg_put(reinterpret_cast<unsigned long long*>(rs_xtab[rs_k]) + rs_me, rs_e, __float_as_uint(rs_mine));",
-            "      const unsigned long long* rs_slots = reinterpret_cast<const unsigned long long*>(rs_xtab[rs_me]);",
+            "        rs_xchg_put(reinterpret_cast<unsigned long long*>(rs_xtab[rs_k]) + rs_bank + rs_me, rs_e,",
+            "                    __float_as_uint(rs_mine));",
+            "      const unsigned long long* rs_slots = reinterpret_cast<const unsigned long long*>(rs_xtab[rs_me]) + rs_bank;",
             f"      {ct} {acc.name} = __uint_as_float(rs_xchg_get(rs_slots, rs_e));",
             "      for (int rs_k = 1; rs_k < RS_R; ++rs_k)",
             f"        {acc.name} = {add(acc.name, '__uint_as_float(rs_xchg_get(rs_slots + rs_k, rs_e))')};",

@@ -76,14 +76,28 @@ class Executable:
             fmad = fmad or bool(chosen.get("fmad", False))
             name_expr = f"{chosen['name']}<{targs}>" if targs else chosen["name"]
             exprs.append(name_expr)
-            self.launches.append((chosen, name_expr))
+            # a template reads / writes its buffers with 16-byte accesses (float4,
+            # bulk copies, TMA): its generic kernel is compiled beside it and runs
+            # instead when a caller's buffer is not 16-byte aligned (e.g. x[1:])
+            fb = chosen.get("fallback") if chosen is st and not (st.get("peer_ranks") or st.get("peer_halo")) \
+                else None
+            if fb is not None:
+                exprs.append(f"{fb['name']}<{targs}>" if targs else fb["name"])
+            self.launches.append((chosen, fb))
         opts = ["--fmad=true" if fmad else "--fmad=false"]
         self.module = rt.load_module(text, exprs, opts, program_name=f"{self.plan['unit']}.cu")
+        lowered = iter(self.module.lowered)
         self.kernels = []
-        for (chosen, name_expr), lowered in zip(self.launches, self.module.lowered):
-            fn = self.module.function(lowered)
+        self._fallbacks = []
+        for chosen, fb in self.launches:
+            fn = self.module.function(next(lowered))
             grid, block, smem, cluster = self._config(chosen)
             self.kernels.append((chosen, fn, grid, block, smem, cluster))
+            if fb is not None:
+                fb_fn = self.module.function(next(lowered))
+                self._fallbacks.append((fb, fb_fn, *self._config(fb)))
+            else:
+                self._fallbacks.append(None)
         self._temps = None
 
     # launch configuration --------------------------------------------------
@@ -136,6 +150,16 @@ class Executable:
                                                           device="cuda")
         return self._temps
 
+    def _stages_for(self, buffers: dict):
+        """The kernels to launch for these buffers: each template stage, or its
+        generic fallback when a caller buffer is not 16-byte aligned."""
+        names = [i["name"] for i in self.plan["inputs"] if not i["scalar"] and not i.get("peer")]
+        names.append(self.plan["output"]["name"])
+        aligned = all(_dptr(buffers[nm]) % 16 == 0 for nm in names if nm in buffers)
+        if aligned:
+            return self.kernels
+        return [fb if fb is not None else k for k, fb in zip(self.kernels, self._fallbacks)]
+
     def launch(self, buffers: dict, stream=None):
         """Launch every stage.  `buffers` maps argument names to device
         tensors / pointers (arrays) or Python numbers (scalar inputs)."""
@@ -150,7 +174,7 @@ class Executable:
                 base_args.append(ctypes.c_float(float(v)) if scalar_types[name] == "float" else ctypes.c_int(int(v)))
             else:
                 base_args.append(ctypes.c_void_p(_dptr(buffers[name])))
-        for st, fn, grid, block, smem, cluster in self.kernels:
+        for st, fn, grid, block, smem, cluster in self._stages_for(buffers):
             args = list(base_args)
             for extra in st.get("extra_args", []):
                 args.append(self._extra_arg(extra, buffers, temps))
@@ -172,7 +196,7 @@ class Executable:
             else:
                 base_args.append(ctypes.c_void_p(_dptr(buffers[name])))
         prepared = []
-        for st, fn, grid, block, smem, cluster in self.kernels:
+        for st, fn, grid, block, smem, cluster in self._stages_for(buffers):
             args = list(base_args) + [self._extra_arg(e, buffers, temps) for e in st.get("extra_args", [])]
             prepared.append(rt.PreparedLaunch(fn, grid, block, args, smem, stream, cluster, _launch_flags(st)))
 

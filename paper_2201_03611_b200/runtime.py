@@ -132,6 +132,54 @@ def _cstr_array(items):
 DEFAULT_OPTS = ("--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-default-device")
 
 _cubin_cache: dict = {}
+_headers_digest = None
+
+
+def _include_digest() -> str:
+    """Hash of the device headers the kernel text includes (part of the
+    cache key: a changed header is a different cubin)."""
+    global _headers_digest
+    if _headers_digest is None:
+        h = hashlib.sha256()
+        for p in sorted(Path(INCLUDE_DIR).rglob("*")):
+            if p.is_file():
+                h.update(p.name.encode())
+                h.update(p.read_bytes())
+        _headers_digest = h.hexdigest()
+    return _headers_digest
+
+
+def cache_dir():
+    """On-disk cubin cache keyed by the source hash (RISE_CUBIN_CACHE; "0"
+    disables it).  Only a compile-time saving: a miss recompiles."""
+    d = os.environ.get("RISE_CUBIN_CACHE", str(Path.home() / ".cache" / "rise_b200" / "cubin"))
+    return None if d == "0" else Path(d)
+
+
+def _disk_get(key):
+    d = cache_dir()
+    if d is None:
+        return None
+    try:
+        blob = (d / f"{key}.cubin").read_bytes()
+        names = (d / f"{key}.names").read_text().split("\n")
+    except OSError:
+        return None
+    return blob, names
+
+
+def _disk_put(key, blob, names):
+    d = cache_dir()
+    if d is None:
+        return
+    try:
+        d.mkdir(parents=True, exist_ok=True)
+        for suffix, data in ((".names", "\n".join(names).encode()), (".cubin", blob)):
+            tmp = d / f"{key}{suffix}.{os.getpid()}.tmp"
+            tmp.write_bytes(data)
+            os.replace(tmp, d / f"{key}{suffix}")  # atomic: concurrent ranks may race
+    except OSError:
+        pass
 
 
 def compile_cubin(source: str, name_exprs, opts=(), program_name="rise.cu"):
@@ -139,10 +187,14 @@ def compile_cubin(source: str, name_exprs, opts=(), program_name="rise.cu"):
     Raises EmitError with the NVRTC log on failure.  Needs no GPU."""
     full_opts = list(DEFAULT_OPTS) + [f"-I{INCLUDE_DIR}"] + list(opts)
     key = hashlib.sha256(
-        "\0".join([source, program_name] + full_opts + list(name_exprs)).encode()
+        "\0".join([source, program_name, _include_digest()] + full_opts + list(name_exprs)).encode()
     ).hexdigest()
     hit = _cubin_cache.get(key)
     if hit is not None:
+        return hit
+    hit = _disk_get(key)
+    if hit is not None and len(hit[1]) == len(name_exprs):
+        _cubin_cache[key] = hit
         return hit
     L = lib()
     image, size = ctypes.c_void_p(), ctypes.c_size_t()
@@ -163,6 +215,7 @@ def compile_cubin(source: str, name_exprs, opts=(), program_name="rise.cu"):
         L.rs_free_host(log)
     out = (blob, lowered)
     _cubin_cache[key] = out
+    _disk_put(key, blob, lowered)
     return out
 
 

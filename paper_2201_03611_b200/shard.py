@@ -218,7 +218,7 @@ class PeerSources:
 
 class PeerExchange:
     """The exchange slots of a `reduce` kernel emitted with peer_ranks=R:
-    every rank owns R zeroed 64-bit slots (CUDA IPC-exported), maps everyone
+    every rank owns 2R zeroed 64-bit slots (two banks, used by epoch parity) (CUDA IPC-exported), maps everyone
     else's, and hands the kernel a device table [slot array of rank 0 .. R-1,
     this rank].  The kernel's last block writes this rank's total into slot
     `rank` of every rank's array (a system-scope release store of
@@ -233,7 +233,8 @@ class PeerExchange:
         from . import runtime
 
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
-        self.slots = torch.zeros(self.world, dtype=torch.int64, device="cuda")
+        # two banks of R slots, by epoch parity (the kernel's rs_bank)
+        self.slots = torch.zeros(2 * self.world, dtype=torch.int64, device="cuda")
         torch.cuda.synchronize()
         everyone = [None] * self.world
         dist.all_gather_object(everyone, runtime.ipc_handle(self.slots.data_ptr()), group=group)

@@ -122,6 +122,9 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
     # stages stay 1024-byte aligned (128B swizzle)
     boxrows_py = f"(-(-({rows_py}) // 8) * 8)"
     stage_py = f"(-(-({len(rs_list) * nbox * 32} * {boxrows_py} + {len(sh_list) * KT}) // 256) * 256)"
+    # one stage (+ the 1024-byte alignment slack and the barriers) must fit the
+    # 227 KiB opt-in shared memory; wider programs take the generic kernel
+    pre.append(f"{stage_py} * 4 + 1024 + 64 <= 227 * 1024")
     # ring depth: up to STAGES, as many as fit two blocks per SM for the block's rows
     # (at least one: a one-stage ring issues each stage just before it waits on it)
     budget = 113 * 1024

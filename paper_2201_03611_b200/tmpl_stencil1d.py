@@ -42,12 +42,14 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     ((iv, N),) = loops
     bounds = _seq_loop_bounds(body)
     abuf, lo, hi = None, None, None
+    unclamped = set()  # buffers also read at indices that are not clamp variables
     for _t, value in lir.stmt_exprs(body):
         for ld in lir.expr_loads(value):
             clamped = [v for v in nat.free_vars(ld.index) if v in prog.clamps]
             if not clamped:
                 if iv in nat.free_vars(ld.index):
                     return None  # another i-dependent stream: the generic kernel keeps it
+                unclamped.add(ld.buf)
                 continue
             buf = prog.buffers[ld.buf]
             if buf.role != "input" or buf.ctype != "float" or len(buf.dims) != 1 or len(ld.indices) != 1:
@@ -66,6 +68,8 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
             hi = rng[1] if hi is None else max(hi, rng[1])
     if abuf is None or not (lo <= 0 <= hi) or hi - lo > 64:
         return None
+    if abuf in unclamped:
+        return None  # e.g. A[0] or A[k] beside the window: only clamped loads are redirected to the tile
     A = prog.buffers[abuf]
     H = A.dims[0]
     r = NatRenderer(prog.clamps)

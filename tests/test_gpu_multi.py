@@ -291,3 +291,75 @@ def test_dot_totals_exchanged_in_peer_memory(world, n):
     for rank, same, kinds in res:
         assert kinds == ["reduce"]
         assert same, f"rank {rank}: exchanged total differs from the rank-order fold"
+
+
+def _bands_worker(rank, world, port, q):
+    """gemv and sgemm row bands (SURVEY.md §8 e C2 / C4) as bench.py runs them
+    strong-scaled: M / A split in row bands, x replicated; the y blocks
+    all-gathered after the GEMV; B owned in 1/world row blocks and
+    all-gathered before the GEMM, the C blocks gathered after it."""
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2201_03611_b200 import emit_cuda, programs, shard
+        from paper_2201_03611_b200.run import Executable
+
+        torch.cuda.set_device(0)
+
+        def gather_rows(block):  # rank-order all-gather (gloo moves host tensors)
+            parts = [None] * world
+            dist.all_gather_object(parts, block.cpu().numpy())
+            return np.concatenate(parts, axis=0)
+
+        # gemv: 300 rows do not split evenly over 3 ranks' 8-row rowfold blocks
+        n, m = 300, 512
+        M = oracle.rng_inputs(2, n, m)
+        x = oracle.rng_inputs(12, m)
+        r0, rows = shard.row_band(n, world, rank)
+        c = programs.compile_config("gemv")
+        exe = Executable(emit_cuda(c.unit), {"n": rows, "m": m})
+        y = exe(torch.from_numpy(np.ascontiguousarray(M[r0:r0 + rows]).reshape(-1)).cuda(),
+                torch.from_numpy(x).cuda())
+        torch.cuda.synchronize()
+        y_all = gather_rows(y)
+        ok_gemv = np.array_equal(y_all, oracle.mv(M, x))
+        gemv_kinds = exe.template_kinds
+
+        # sgemm: B (as Bt) replicated by an all-gather of 1/world row blocks
+        n, mm, k = 256, 384, 512
+        A = oracle.rng_inputs(4, n, k)
+        Bt = oracle.rng_inputs(14, mm, k)
+        b0, brows = shard.row_band(mm, world, rank)
+        Bt_full = torch.from_numpy(gather_rows(torch.from_numpy(Bt[b0:b0 + brows]))).reshape(-1).cuda()
+        r0, rows = shard.row_band(n, world, rank)
+        c = programs.compile_config("sgemm")
+        exe = Executable(emit_cuda(c.unit), {"n": rows, "m": mm, "k": k})
+        C = exe(torch.from_numpy(np.ascontiguousarray(A[r0:r0 + rows]).reshape(-1)).cuda(), Bt_full)
+        torch.cuda.synchronize()
+        C_all = gather_rows(C.view(rows, mm)).reshape(n, mm)
+        C64, absC = oracle.sgemm_bt_f64(A, Bt)
+        ok_sgemm = bool(np.all(np.abs(C_all - C64) <= oracle.gemm_bound(k, absC)))
+        q.put((rank, ok_gemv, gemv_kinds, ok_sgemm, exe.template_kinds))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gemv_sgemm_row_bands_with_gathers(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bands_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok_gemv, gemv_kinds, ok_sgemm, sgemm_kinds in res:
+        assert ok_gemv, f"rank {rank}: gathered gemv differs from the oracle"
+        assert gemv_kinds == ["rowfold"]
+        assert ok_sgemm, f"rank {rank}: gathered sgemm outside the 3xTF32 bound"
+        assert sgemm_kinds == ["gemm_tc"]

@@ -558,8 +558,14 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
 }
 
 // Persistent form of gemm_3xtf32_2sm: one CTA pair per SM pair, looping over
-// the same work units (whole tiles, then the K-split tail units) — unit u
-// goes to pair u % P, so each pair owns at most one split unit, its last.
+// the same work units (whole tiles, then the K-split units) — unit u goes to
+// pair u % P, so each pair owns at most one split unit, its last.  A split
+// tile is cut into `ksplit` K ranges (2 for the tail past the last whole
+// wave; up to 4 when the whole GEMM has fewer tiles than SM pairs, e.g. the
+// 512-row A blocks of a strong-scaled multi-GPU sgemm): parts 1.. park their
+// partial tiles in `ws` and count themselves into the tile's flag (release);
+// part 0 waits for all of them (acquire) and stores
+// C = ((part0 + part1) + part2) + ... — a fixed order, deterministic.
 // The accumulator is double-buffered in TMEM (2 x BN columns): the MMA
 // issuer fills slot i & 1 while four dedicated epilogue warps drain the
 // other, so a tile's epilogue and the next tile's prologue overlap its
@@ -572,7 +578,7 @@ constexpr int PTHREADS = 320;
 
 template <int M, int N, int K, int BN, int STAGES, bool B_MN = false, int GROUP_M = 0>
 RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const rs_tmap* mapA, const rs_tmap* mapB,
-                                          int n_full, int n_units, float* __restrict__ ws,
+                                          int n_full, int n_units, int ksplit, float* __restrict__ ws,
                                           unsigned* __restrict__ flags) {
   using G = Cfg2<BN, STAGES>;
   extern __shared__ __align__(1024) unsigned char rs_gemm_smem_raw[];
@@ -596,14 +602,15 @@ RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const 
   auto a_lo = [&](int s) { return smem + s * G::STAGE_BYTES + G::TILE_A; };
   auto b_raw = [&](int s) { return smem + s * G::STAGE_BYTES + 2 * G::TILE_A; };
   auto b_lo = [&](int s) { return smem + s * G::STAGE_BYTES + 2 * G::TILE_A + G::TILE_B; };
-  // unit -> (tile, K range, split half)
+  // unit -> (tile, K range, split part; sidx = the split tile's index or -1)
   auto unit_of = [&](int u, int& m0, int& n0, int& kb0, int& kb1, int& khalf, int& sidx) {
     const bool split = u >= n_full;
-    sidx = split ? u - n_full : -1;
-    const int tile = split ? n_full + (sidx >> 1) : u;
-    khalf = split ? (sidx & 1) : 0;
-    kb0 = split && khalf ? KB / 2 : 0;
-    kb1 = split && !khalf ? KB / 2 : KB;
+    const int su = split ? u - n_full : 0;
+    sidx = split ? su / ksplit : -1;
+    const int tile = split ? n_full + sidx : u;
+    khalf = split ? su % ksplit : 0;
+    kb0 = split ? (KB * khalf) / ksplit : 0;
+    kb1 = split ? (KB * (khalf + 1)) / ksplit : KB;
     if (GROUP_M > 0) {  // tiles in groups of GROUP_M row tiles, column by column (L2 reuse of A and B)
       constexpr int NTM = (M + 255) / 256;
       const int grp = tile / (GROUP_M * NTN), r = tile % (GROUP_M * NTN);
@@ -745,13 +752,16 @@ RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const 
           if (col + 3 < ncols) crow[col + 3] = v.w;
         }
       };
-      float* wrow = ws + ((long long)(split ? sidx >> 1 : 0) * 256 + trow) * BN;
-      unsigned* flag = flags + 2 * (split ? sidx >> 1 : 0) + rank;
+      // parked parts of split tile sidx: part p (1 .. ksplit-1) at slot sidx * (ksplit-1) + p - 1
+      const long long part_stride = 256LL * BN;
+      float* wbase = ws + ((long long)(split ? sidx : 0) * (ksplit - 1)) * part_stride + (long long)trow * BN;
+      float* wrow = wbase + (long long)(khalf > 0 ? khalf - 1 : 0) * part_stride;
+      unsigned* flag = flags + 2 * (split ? sidx : 0) + rank;
       if (split && khalf == 0) {
         unsigned v;
         do {
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-        } while (v == 0u);
+        } while (v < (unsigned)(ksplit - 1));
       }
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -762,7 +772,7 @@ RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const 
           for (int j = 0; j < 32; j += 4)
             store4(c0 + j, make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
                                        __uint_as_float(r[j + 3])));
-        } else if (khalf == 1) {
+        } else if (khalf > 0) {
 #pragma unroll
           for (int j = 0; j < 32; j += 4)
             __stcg(reinterpret_cast<float4*>(wrow + c0 + j),
@@ -771,20 +781,24 @@ RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const 
         } else {
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
-            const float4 w = __ldcg(reinterpret_cast<const float4*>(wrow + c0 + j));
-            store4(c0 + j, make_float4(__fadd_rn(__uint_as_float(r[j]), w.x), __fadd_rn(__uint_as_float(r[j + 1]), w.y),
-                                       __fadd_rn(__uint_as_float(r[j + 2]), w.z),
-                                       __fadd_rn(__uint_as_float(r[j + 3]), w.w)));
+            float4 a = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                                   __uint_as_float(r[j + 3]));
+#pragma unroll 1
+            for (int p = 1; p < ksplit; ++p) {  // parts in order: deterministic
+              const float4 w = __ldcg(reinterpret_cast<const float4*>(wbase + (long long)(p - 1) * part_stride + c0 + j));
+              a = make_float4(__fadd_rn(a.x, w.x), __fadd_rn(a.y, w.y), __fadd_rn(a.z, w.z), __fadd_rn(a.w, w.w));
+            }
+            store4(c0 + j, a);
           }
         }
       }
-      // this CTA's share of the slot is drained (and the parked tile used)
+      // this CTA's share of the slot is drained (and the parked tiles used)
       fence_before();
       asm volatile("bar.sync 2, 128;" ::: "memory");
       if (t == 0) {
-        if (split && khalf == 1) {
+        if (split && khalf > 0) {
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(1u) : "memory");
+          asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(flag), "r"(1u) : "memory");
         } else if (split) {
           *flag = 0u;
         }

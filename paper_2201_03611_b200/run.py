@@ -235,17 +235,14 @@ class Executable:
             if table is None:
                 raise InterpreterError("peer-source kernel launched without buffers['rs_peer_table']")
             return ctypes.c_void_p(_dptr(table))
-        if kind == "gemm_units":
-            from .tmpl_gemm import full_tiles, pair_tiles
+        if kind in ("gemm_units", "gemm_full_tiles", "gemm_ksplit"):
+            from .tmpl_gemm import schedule, work_units
 
             M, N, K = (eval_py(extra[k], self.nats) for k in ("M", "N", "K"))
-            nfull = full_tiles(M, N, K, extra["bn"], self.sm_count)
-            return ctypes.c_int(nfull + 2 * (pair_tiles(M, N, extra["bn"]) - nfull))
-        if kind == "gemm_full_tiles":
-            from .tmpl_gemm import full_tiles
-
-            return ctypes.c_int(full_tiles(eval_py(extra["M"], self.nats), eval_py(extra["N"], self.nats),
-                                           eval_py(extra["K"], self.nats), extra["bn"], self.sm_count))
+            if kind == "gemm_units":
+                return ctypes.c_int(work_units(M, N, K, extra["bn"], self.sm_count))
+            nfull, s = schedule(M, N, K, extra["bn"], self.sm_count)
+            return ctypes.c_int(nfull if kind == "gemm_full_tiles" else s)
         raise InterpreterError(f"unknown extra kernel argument {kind!r}")
 
     def run_host(self, host_inputs, host_out, device_inputs, device_out, stream=None, extra=None):

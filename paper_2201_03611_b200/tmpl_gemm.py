@@ -91,12 +91,12 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
     if PAIR:
         extra += ["int rs_nfull", "float* __restrict__ rs_ws", "unsigned* __restrict__ rs_flags"]
         if PERSIST:
-            extra.insert(3, "int rs_nunits")
+            extra[3:3] = ["int rs_nunits", "int rs_ksplit"]
     threads = 320 if (PAIR and PERSIST) else 192
     lines = kernel_head(prog, name, temps, launch_bounds=f"{threads}, 1", extra_params=extra)
     if PAIR:
         fn = "gemm_3xtf32_2sm_persistent" if PERSIST else "gemm_3xtf32_2sm"
-        args = "rs_nfull, rs_nunits, rs_ws, rs_flags" if PERSIST else "rs_nfull, rs_ws, rs_flags"
+        args = "rs_nfull, rs_nunits, rs_ksplit, rs_ws, rs_flags" if PERSIST else "rs_nfull, rs_ws, rs_flags"
         lines += [
             f"  rise_gemm::{fn}<{r(M)}, {r(N)}, {r(K)}, {PAIR_BN}, {PAIR_STAGES}, "
             f"{'true' if b_mn else 'false'}{(', ' + str(GROUP_M)) if PERSIST and GROUP_M else ''}>"
@@ -114,7 +114,8 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
             "b_major": "mn" if b_mn else "k",
             "persistent": PERSIST,
             "fmad": False,
-            "order": "3xtf32 tensor-core, CTA pairs; tail tiles K-split in two halves (reassociated)",
+            "order": ("3xtf32 tensor-core, CTA pairs; tail tiles K-split in two halves, or every tile in up to 4 "
+                      "K ranges when there are fewer tiles than SM pairs (reassociated)"),
             # ragged M / N / K: TMA zero-fill + a guarded epilogue; the 16-byte
             # row pitch of the TMA views needs K % 4 (and N % 4 for MN-major B)
             "pre": [f"({py_expr(K)}) % 4 == 0", f"({py_expr(M)}) * ({py_expr(N)}) * ({py_expr(K)}) > 0"]
@@ -128,12 +129,13 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
                  {"kind": "tma2d", "buf": b_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(N)],
                   "pitch": py_expr(K), "box": [32, PAIR_BN // 2], "swizzle": 3}),
                 {"kind": "gemm_full_tiles", "M": py_expr(M), "N": py_expr(N), "K": py_expr(K), "bn": PAIR_BN},
-                *([{"kind": "gemm_units", "M": py_expr(M), "N": py_expr(N), "K": py_expr(K), "bn": PAIR_BN}]
+                *([{"kind": "gemm_units", "M": py_expr(M), "N": py_expr(N), "K": py_expr(K), "bn": PAIR_BN},
+                   {"kind": "gemm_ksplit", "M": py_expr(M), "N": py_expr(N), "K": py_expr(K), "bn": PAIR_BN}]
                   if PERSIST else []),
                 {"kind": "workspace", "name": f"rs_ws_{base_name}_ktail"},
                 {"kind": "workspace", "name": f"rs_ws_{base_name}_kflags"},
             ],
-            # K-split tail tiles park their second halves here (<= one wave of pair tiles)
+            # K-split tiles park their parts 1.. here: (parts - 1) x split tiles <= one wave of pair tiles
             "workspace": [{"name": f"rs_ws_{base_name}_ktail", "ctype": "float", "size": f"74 * 256 * {PAIR_BN}"},
                           {"name": f"rs_ws_{base_name}_kflags", "ctype": "int", "size": "2 * 74"}],
         }
@@ -171,18 +173,39 @@ def pair_tiles(M, N, bn):
     return -(-M // 256) * -(-N // bn)
 
 
-def full_tiles(M, N, K, bn, sm):
-    """How many 256 x bn pair tiles run whole.  The tail past the last whole
-    wave of SM pairs is split along K into two units per tile when those
-    units fit in one wave (else nothing is split).  RISE_GEMM_KSPLIT=0
-    disables the split."""
+def schedule(M, N, K, bn, sm, persistent=PERSIST):
+    """(whole tiles, K parts per split tile).  Whole tiles run first; the rest
+    are split along K so the last wave fills the SM pairs:
+      * at least a wave of tiles: the tail past the last whole wave is split in
+        two when those units fit in one wave (else nothing is split);
+      * fewer tiles than SM pairs (e.g. the 512-row A block of an 8-GPU
+        strong-scaled 4096^3 sgemm: 32 tiles on 74 pairs): every tile is split
+        in S = min(4, pairs // tiles) K ranges (persistent kernel only).
+    Each K range keeps >= 2 K blocks of 32.  RISE_GEMM_KSPLIT=0 disables it."""
     tiles = pair_tiles(M, N, bn)
     slots = max(1, sm // 2)
+    kb = -(-K // 32)
+    if os.environ.get("RISE_GEMM_KSPLIT", "1") != "1" or tiles == 0 or kb < 2:
+        return tiles, 1
+    if tiles < slots:
+        s = min(4, slots // tiles, kb // 2) if persistent else 1
+        while s > 1 and tiles * (s - 1) > SPLIT_SLOTS_MAX:  # the parked parts' workspace
+            s -= 1
+        return (0, s) if s >= 2 else (tiles, 1)
     tail = tiles % slots
-    if (os.environ.get("RISE_GEMM_KSPLIT", "1") != "1" or tail == 0 or tiles < slots or 2 * tail > slots
-            or tail > SPLIT_SLOTS_MAX or -(-K // 32) < 2):
-        return tiles
-    return tiles - tail
+    if tail == 0 or 2 * tail > slots or tail > SPLIT_SLOTS_MAX:
+        return tiles, 1
+    return tiles - tail, 2
+
+
+def full_tiles(M, N, K, bn, sm):
+    """How many 256 x bn pair tiles run whole (schedule())."""
+    return schedule(M, N, K, bn, sm)[0]
+
+
+def work_units(M, N, K, bn, sm):
+    nfull, s = schedule(M, N, K, bn, sm)
+    return nfull + s * (pair_tiles(M, N, bn) - nfull)
 
 
 def launch(st, nats, sm):
@@ -192,9 +215,10 @@ def launch(st, nats, sm):
     N = eval_py(st["N"], nats)
     if st.get("pair"):
         K = eval_py(st["K"], nats)
-        tiles = pair_tiles(M, N, st["bn"])
-        nfull = full_tiles(M, N, K, st["bn"], sm)
-        units = nfull + 2 * (tiles - nfull)
+        nfull, s = schedule(M, N, K, st["bn"], sm, st.get("persistent", False))
+        if not st.get("persistent") and s != 2:
+            nfull = pair_tiles(M, N, st["bn"])  # the non-persistent kernel splits tail tiles in two only
+        units = nfull + max(s, 2) * (pair_tiles(M, N, st["bn"]) - nfull)
         if st.get("persistent"):  # one pair per SM pair, looping over the units
             return (2 * max(1, min(units, sm // 2)), 1, 1), (320, 1, 1), st["smem"], (2, 1, 1)
         return (2 * units, 1, 1), (192, 1, 1), st["smem"], (2, 1, 1)

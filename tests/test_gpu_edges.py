@@ -160,3 +160,34 @@ def test_memcpy_peer_same_device(gpu):
     assert torch.equal(dst, src)
     with pytest.raises(Exception):
         gpu.memcpy_peer(dst.data_ptr(), 0, src.data_ptr(), 99, 4, stream)
+
+
+def test_misaligned_views_take_the_generic_kernel(gpu):
+    """Templates read with 16-byte accesses (float4, bulk copies, TMA); a
+    caller's view at a 4-byte offset (x[1:]) runs the stage's generic kernel
+    instead of faulting — same results (gemv: bit-exact; dot: the generic
+    kernel is the reference's own left fold)."""
+    import torch
+
+    c = _cfg("gemv")
+    n, m = 64, 256
+    M = oracle.rng_inputs(2, n, m)
+    x = oracle.rng_inputs(3, m)
+    exe = Executable(emit_cuda(c.unit), {"n": n, "m": m})
+    Mbig = torch.zeros(n * m + 1, dtype=torch.float32, device="cuda")
+    Mbig[1:] = torch.from_numpy(M.reshape(-1)).cuda()
+    y = exe(Mbig[1:], torch.from_numpy(x).cuda())
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy(), oracle.mv(M, x))
+
+    c = _cfg("dot")
+    a = oracle.rng_inputs(1, 4097)
+    b = oracle.rng_inputs(2, 4096)
+    exe = Executable(emit_cuda(c.unit), {"n": 4096})
+    got = exe(torch.from_numpy(a).cuda()[1:], torch.from_numpy(b).cuda())
+    torch.cuda.synchronize()
+    assert got.cpu().numpy()[0] == oracle.dot(a[1:], b)
+    out = torch.empty(2, dtype=torch.float32, device="cuda")
+    got = exe(torch.from_numpy(a[1:].copy()).cuda(), torch.from_numpy(b).cuda(), out=out[1:])
+    torch.cuda.synchronize()
+    assert got.cpu().numpy()[0] == oracle.dot(a[1:], b)

@@ -57,7 +57,7 @@ def _match_seqfold(prog, stage, base_name, temps, exact):
 
 
 def match(prog, stage, base_name, temps, exact, reassociate=True):
-    for matcher in (_match_gemm, _match_rowfold, _match_reduce, _match_stencil, _match_allpairs,
+    for matcher in (_match_gemm, _match_gemm_tiled, _match_rowfold, _match_reduce, _match_stencil, _match_allpairs,
                     _match_seqfold, _match_iterate, _match_transpose, _match_stencil1d):
         if not reassociate and matcher.__name__ not in ORDER_PRESERVING:
             continue
@@ -69,6 +69,17 @@ def match(prog, stage, base_name, temps, exact, reassociate=True):
 
 def _match_gemm(prog, stage, base_name, temps, exact):
     out = tmpl_gemm.match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape)
+    if out is None:
+        return None
+    text, plan = out
+    return IdiomKernel(plan["name"], text, plan, includes=["rise/gemm_tc.cuh"])
+
+
+def _match_gemm_tiled(prog, stage, base_name, temps, exact):
+    """The tiled sgemm program (programs.SGEMM_TILED): workgroups over row
+    blocks of A staged in Local memory, work-items over columns, K in tiles —
+    recognised as the same contraction and run on the tensor cores."""
+    out = tmpl_gemm.match_tiled(prog, stage, base_name, temps, exact, fold_shape)
     if out is None:
         return None
     text, plan = out

@@ -13,7 +13,9 @@ front end (`frontend.compile_program`) and then the sm100a back end.
 * C3 `conv`  — 3x3 stencil: padClamp2D + slide2D + map/reduce (SURVEY.md
                §8.1 validated form), weights as an Array[3, Array[3, f32]].
 * C4 `sgemm` — A x B with B given transposed (`Bt`), the form the reference
-               can already translate and emit (SURVEY.md §8 c, C4).
+               can already translate and emit (SURVEY.md §8 c, C4); and
+               `sgemm_tiled`, the tiled split / transpose / toMem(Local)
+               lowering BASELINE.json names.
 * C5 `nbody` — all-pairs accelerations + Euler velocity update (one step),
                positions Array[n, Array[3, f32]] and masses Array[n, f32].
 """
@@ -109,6 +111,37 @@ def sgemm = depFun((n: Nat, m: Nat, k: Nat) =>
       zip(arow)(bcol) |> reduceSeq(Private)(fun(acc, p => acc + fst(p) * snd(p)))(0.0f) ))) ))))
 """
 
+# C4 as BASELINE.json names it: the tiled lowering.  Work-groups take row
+# blocks of A (split(2)); each stages its block in Local memory (toMem(Local),
+# the work-items copying each row together); the work-items then
+# walk the columns of B (read through transpose: B is row-major K x N), and
+# each output is folded over K in tiles of 32 (split(32)): per-tile partial
+# dot products, then their sum.  Needs 2 | n and 32 | k (SGEMM_TILED_ASSUMPTIONS).
+# The generic kernel runs it in exactly this order (bit-exact with the
+# reference semantics); the gemm_tc template recognises the same contraction
+# through the staging and the K tiles (tmpl_gemm.match_tiled) and runs it on
+# the tensor cores (3xTF32, fp64 error bound).
+SGEMM_TILED = """\
+def sgemmTiled = depFun((n: Nat, m: Nat, k: Nat) =>
+  fun(A: Array[n, Array[k, f32]] => fun(B: Array[k, Array[m, f32]] =>
+    A |> split(2) |> mapWorkGroup(fun(aBlock =>
+      aBlock |> mapSeq(fun(arow => arow |> mapLocal(fun(v => v * 1.0f)))) |> toMem(Local) |> fun(aLocal =>
+        aLocal |> mapSeq(fun(arow =>
+          transpose(B) |> mapLocal(fun(bcol =>
+            zip(arow)(bcol) |> split(32)
+              |> mapSeq(fun(tile => tile |> reduceSeq(Private)(fun(acc, p => acc + fst(p) * snd(p)))(0.0f)))
+              |> toMem(Private)
+              |> reduceSeq(Private)(fun(acc, v => acc + v))(0.0f) )) )) ) )) |> join )))
+"""
+SGEMM_TILE_ROWS, SGEMM_TILE_K = 2, 32
+
+
+def sgemm_tiled_assumptions():
+    from ._ref import nat
+
+    return ((nat.Var("n"), nat.Const(SGEMM_TILE_ROWS)), (nat.Var("k"), nat.Const(SGEMM_TILE_K)))
+
+
 # the same step for a block of t target bodies against all n sources (the
 # per-GPU program of the multi-GPU decomposition, shard.sharded_nbody)
 NBODY_SHARD = """\
@@ -132,6 +165,8 @@ CONFIGS = {
     "conv": dict(source=CONV, strategy=None, name="conv", nats={"n": 8192, "m": 8192}),
     "sgemm": dict(source=SGEMM_BT, strategy=None, name="sgemm", nats={"n": 4096, "m": 4096, "k": 4096}),
     "nbody": dict(source=NBODY, strategy=None, name="nbody", nats={"n": 131072}),
+    "sgemm_tiled": dict(source=SGEMM_TILED, strategy=None, name="sgemmTiled",
+                        nats={"n": 4096, "m": 4096, "k": 4096}, assumptions=sgemm_tiled_assumptions),
 }
 
 
@@ -139,4 +174,5 @@ def compile_config(key: str):
     from .frontend import compile_program
 
     cfg = CONFIGS[key]
-    return compile_program(cfg["source"], cfg["strategy"], name=cfg["name"])
+    asm = cfg.get("assumptions")
+    return compile_program(cfg["source"], cfg["strategy"], name=cfg["name"], assumptions=asm() if asm else ())

@@ -79,26 +79,33 @@ class Executable:
             # a template reads / writes its buffers with 16-byte accesses (float4,
             # bulk copies, TMA): its generic kernel is compiled beside it and runs
             # instead when a caller's buffer is not 16-byte aligned (e.g. x[1:])
+            # (compiled on first use: some generic kernels only compile at small sizes)
             fb = chosen.get("fallback") if chosen is st and not (st.get("peer_ranks") or st.get("peer_halo")) \
                 else None
-            if fb is not None:
-                exprs.append(f"{fb['name']}<{targs}>" if targs else fb["name"])
-            self.launches.append((chosen, fb))
-        opts = ["--fmad=true" if fmad else "--fmad=false"]
-        self.module = rt.load_module(text, exprs, opts, program_name=f"{self.plan['unit']}.cu")
-        lowered = iter(self.module.lowered)
+            self.launches.append((chosen, name_expr, fb))
+        self._opts = ["--fmad=true" if fmad else "--fmad=false"]
+        self.module = rt.load_module(text, exprs, self._opts, program_name=f"{self.plan['unit']}.cu")
         self.kernels = []
-        self._fallbacks = []
-        for chosen, fb in self.launches:
-            fn = self.module.function(next(lowered))
+        for (chosen, _e, _fb), lowered in zip(self.launches, self.module.lowered):
+            fn = self.module.function(lowered)
             grid, block, smem, cluster = self._config(chosen)
             self.kernels.append((chosen, fn, grid, block, smem, cluster))
-            if fb is not None:
-                fb_fn = self.module.function(next(lowered))
-                self._fallbacks.append((fb, fb_fn, *self._config(fb)))
-            else:
-                self._fallbacks.append(None)
+        self._fallbacks = {}
+        self._targs = targs
         self._temps = None
+
+    def _fallback(self, k):
+        """Stage k's generic kernel (None for a stage without one)."""
+        if k not in self._fallbacks:
+            fb = self.launches[k][2]
+            entry = None
+            if fb is not None:
+                expr = f"{fb['name']}<{self._targs}>" if self._targs else fb["name"]
+                mod = rt.load_module(self.text, [expr], self._opts, program_name=f"{self.plan['unit']}.cu")
+                entry = (fb, mod.function(mod.lowered[0]), *self._config(fb))
+                self._fallback_modules = getattr(self, "_fallback_modules", []) + [mod]
+            self._fallbacks[k] = entry
+        return self._fallbacks[k]
 
     # launch configuration --------------------------------------------------
     def _config(self, st):
@@ -158,7 +165,11 @@ class Executable:
         aligned = all(_dptr(buffers[nm]) % 16 == 0 for nm in names if nm in buffers)
         if aligned:
             return self.kernels
-        return [fb if fb is not None else k for k, fb in zip(self.kernels, self._fallbacks)]
+        out = []
+        for k, kern in enumerate(self.kernels):
+            fb = self._fallback(k) if kern[0].get("fallback") is not None else None
+            out.append(fb if fb is not None else kern)
+        return out
 
     def launch(self, buffers: dict, stream=None):
         """Launch every stage.  `buffers` maps argument names to device

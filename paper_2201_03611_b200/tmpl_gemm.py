@@ -39,6 +39,8 @@ PERSIST = os.environ.get("RISE_GEMM_PERSIST", "1") == "1"  # measured 278 -> 284
 
 
 def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
+    """The flat nest (programs.SGEMM_BT / SGEMM): two parallel loops over the
+    output and one fold over K."""
     loops, body = parallel_rows(stage)
     if loops is None or len(loops) != 2 or stage.kind != "grid":
         return None
@@ -47,43 +49,227 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
     if shape is None:
         return None
     acc, init, loop, post = shape
-    if not (isinstance(init.value, lir.Lit) and init.value.text in ("0.0f", "0f", "0.0")):
+    if not _zero(init.value):
         return None
-    p, K = loop.var, loop.bound
-    step = loop.body.value
+    step = _product_step(loop.body.value, acc)
+    if step is None:
+        return None
+    if len(post) != 1:
+        return None
+    V = nat.Var
+    desc = _operands(prog, step[0], step[1], V(iv), V(jv), V(loop.var), M, N, loop.bound, post[0])
+    if desc is None or desc["value"] != acc:
+        return None
+    return emit(prog, desc, base_name, temps)
+
+
+def _zero(value):
+    return isinstance(value, lir.Lit) and value.text in ("0.0f", "0f", "0.0")
+
+
+def _product_step(step, acc):
+    """acc + x * y (fp32, two loads) -> (x, y)."""
     if not (isinstance(step, lir.Bin) and step.op == "+" and step.a == acc and isinstance(step.b, lir.Bin)
             and step.b.op == "*" and isinstance(step.b.a, lir.Load) and isinstance(step.b.b, lir.Load)
             and step.ctype == "float"):
         return None
-    x, y = step.b.a, step.b.b
-    V = nat.Var
+    return step.b.a, step.b.b
 
-    def is_row(ld, var):
-        return nat.equal(ld.index, nat.normalize(V(var) * K + V(p)), prog.assumptions)
 
-    def is_col(ld, var):  # B[k][j] of a row-major K x N matrix (e.g. read through transpose(B))
-        return nat.equal(ld.index, nat.normalize(V(p) * N + V(var)), prog.assumptions)
+def _operands(prog, x, y, I, J, P, M, N, K, store):
+    """Which load is A[I][P] and which B (as Bt[J][P], K-major, or B[P][J],
+    MN-major), with the result stored at output[I][J]; None otherwise."""
+
+    def idx(ld):
+        return ld.index
+
+    def is_row(ld, row):
+        return nat.equal(idx(ld), nat.normalize(row * K + P), prog.assumptions)
+
+    def is_col(ld):  # B[k][j] of a row-major K x N matrix (e.g. read through transpose(B))
+        return nat.equal(idx(ld), nat.normalize(P * N + J), prog.assumptions)
 
     b_mn = False  # B is MN-major in shared memory (UMMA b_major = 1)
-    if is_row(x, iv) and is_row(y, jv):
+    if is_row(x, I) and is_row(y, J):
         a_ld, b_ld = x, y
-    elif is_row(y, iv) and is_row(x, jv):
+    elif is_row(y, I) and is_row(x, J):
         a_ld, b_ld = y, x
-    elif PAIR and is_row(x, iv) and is_col(y, jv):
+    elif PAIR and is_row(x, I) and is_col(y):
         a_ld, b_ld, b_mn = x, y, True
-    elif PAIR and is_row(y, iv) and is_col(x, jv):
+    elif PAIR and is_row(y, I) and is_col(x):
         a_ld, b_ld, b_mn = y, x, True
     else:
         return None
     for ld in (a_ld, b_ld):
-        if prog.buffers[ld.buf].role != "input":
+        if prog.buffers[ld.buf].role != "input" or ld.ctype != "float":
             return None
-    if len(post) != 1:
+    if not (isinstance(store, lir.Assign) and isinstance(store.target, lir.Store)
+            and nat.equal(store.target.index, nat.normalize(I * N + J), prog.assumptions)):
         return None
-    st = post[0]
-    if not (isinstance(st, lir.Assign) and isinstance(st.target, lir.Store) and st.value == acc
-            and nat.equal(st.target.index, nat.normalize(V(iv) * N + V(jv)), prog.assumptions)):
+    return {"M": M, "N": N, "K": K, "a": a_ld.buf, "b": b_ld.buf, "b_mn": b_mn, "out": store.target.buf,
+            "value": store.value}
+
+
+# ---------------------------------------------------------------------------
+# the tiled nest (programs.SGEMM_TILED): workgroups over row blocks of A, the
+# block staged in Local memory, work-items over the columns, K in tiles
+
+
+def _copy_nest(stmt):
+    """(Par)For nest ending in L[dst] = S[src] (or S[src] * 1.0f): returns
+    (L, S, dst, src, [(var, bound)]) or None."""
+    loops = []
+    while isinstance(stmt, (lir.For, lir.ParFor)):
+        if isinstance(stmt, lir.ParFor) and stmt.kind != "local":
+            return None
+        loops.append((stmt.var, stmt.bound))
+        stmt = stmt.body
+    if not (isinstance(stmt, lir.Assign) and isinstance(stmt.target, lir.Store)):
         return None
+    v = stmt.value
+    if isinstance(v, lir.Bin) and v.op == "*":
+        if isinstance(v.b, lir.Lit) and v.b.text == "1.0f":
+            v = v.a
+        elif isinstance(v.a, lir.Lit) and v.a.text == "1.0f":
+            v = v.b
+    if not isinstance(v, lir.Load):
+        return None
+    return stmt.target.buf, v.buf, stmt.target.index, v.index, loops
+
+
+def _staged(prog, stmt, allocs):
+    """Peel Local staging buffers: Alloc(L, Local){ Seq[copy into L, rest] }.
+    Returns (compute statement, {L: (source buffer, offset Nat)}) or None."""
+    stage_map = {}
+    while True:
+        if isinstance(stmt, lir.Alloc) and stmt.space == "Local" and stmt.dims:
+            allocs[stmt.name] = stmt
+            stmt = stmt.body
+            continue
+        if isinstance(stmt, lir.Seq) and len(stmt.stmts) >= 2:
+            info = _copy_nest(stmt.stmts[0])
+            if info is None or info[0] not in allocs:
+                return None
+            L, src, dst, sidx, loops = info
+            # the copy visits every element of L once, in row-major order ...
+            size = nat.Const(1)
+            expect = nat.Const(0)
+            for var, bound in loops:
+                expect = expect * bound + nat.Var(var)
+                size = size * bound
+            dims = allocs[L].dims
+            total = nat.Const(1)
+            for d in dims:
+                total = total * d
+            if not (nat.equal(nat.normalize(dst), nat.normalize(expect), prog.assumptions)
+                    and nat.equal(nat.normalize(size), nat.normalize(total), prog.assumptions)):
+                return None
+            # ... from a contiguous run of the source: L[e] == S[e + delta]
+            delta = nat.normalize(sidx - dst, prog.assumptions)
+            if nat.free_vars(delta) & {v for v, _ in loops}:
+                return None
+            if prog.buffers[src].role != "input" or src in stage_map:
+                return None
+            stage_map[L] = (src, delta)
+            rest = stmt.stmts[1:]
+            stmt = rest[0] if len(rest) == 1 else lir.Seq(list(rest))
+            continue
+        return stmt, stage_map
+
+
+def _through_staging(ld, stage_map, assumptions):
+    if ld.buf in stage_map:
+        src, delta = stage_map[ld.buf]
+        return lir.Load(src, nat.normalize(ld.index + delta, assumptions), ld.ctype)
+    return ld
+
+
+def _k_fold(prog, body, fold_shape):
+    """The per-output fold: either acc = 0; for p < K: acc += x*y; store — or
+    K in tiles: P[t] = (fold over kk < TK of x*y) for t < T, then
+    acc = 0; for t < T: acc += P[t]; store.  Returns (x, y, P expr, K, store,
+    the stored accumulator)."""
+    shape = fold_shape(body)
+    if shape is not None:
+        acc, init, loop, post = shape
+        step = _product_step(loop.body.value, acc)
+        if not _zero(init.value) or step is None or len(post) != 1:
+            return None
+        return step[0], step[1], nat.Var(loop.var), loop.bound, post[0], acc
+    if not (isinstance(body, lir.Alloc) and body.space == "Private" and len(body.dims) == 1):
+        return None
+    parts = body.name
+    T = body.dims[0]
+    stmts = body.body.stmts if isinstance(body.body, lir.Seq) else [body.body]
+    if len(stmts) != 2 or not isinstance(stmts[0], lir.For) or not nat.equal(stmts[0].bound, T, prog.assumptions):
+        return None
+    t = stmts[0].var
+    inner = fold_shape(stmts[0].body)
+    if inner is None:
+        return None
+    acc, init, loop, post = inner
+    step = _product_step(loop.body.value, acc)
+    if not _zero(init.value) or step is None or len(post) != 1:
+        return None
+    p0 = post[0]
+    if not (isinstance(p0, lir.Assign) and isinstance(p0.target, lir.Store) and p0.target.buf == parts
+            and nat.equal(p0.target.index, nat.Var(t)) and p0.value == acc):
+        return None
+    outer = fold_shape(stmts[1])
+    if outer is None:
+        return None
+    acc2, init2, loop2, post2 = outer
+    v = loop2.body.value
+    if not (_zero(init2.value) and isinstance(v, lir.Bin) and v.op == "+" and v.a == acc2
+            and isinstance(v.b, lir.Load) and v.b.buf == parts and nat.equal(v.b.index, nat.Var(loop2.var))
+            and nat.equal(loop2.bound, T, prog.assumptions) and len(post2) == 1):
+        return None
+    TK = loop.bound
+    P = nat.normalize(TK * nat.Var(t) + nat.Var(loop.var))
+    return step[0], step[1], P, nat.normalize(T * TK, prog.assumptions), post2[0], acc2
+
+
+def match_tiled(prog, stage, base_name, temps, exact, fold_shape):
+    if stage.kind != "workgroup" or not PAIR:
+        return None
+    wg = stage.stmt
+    got = _staged(prog, wg.body, {})
+    if got is None:
+        return None
+    compute, stage_map = got
+    chain = []
+    s = compute
+    while isinstance(s, (lir.For, lir.ParFor)) and len(chain) < 2:
+        if isinstance(s, lir.ParFor) and s.kind != "local":
+            return None
+        chain.append(s)
+        s = s.body
+    if len(chain) != 2 or not any(isinstance(c, lir.ParFor) for c in chain):
+        return None
+    fold = _k_fold(prog, s, fold_shape)
+    if fold is None:
+        return None
+    x, y, P, K, store, _acc = fold
+    x = _through_staging(x, stage_map, prog.assumptions)
+    y = _through_staging(y, stage_map, prog.assumptions)
+    V = nat.Var
+    for row, col in ((chain[0], chain[1]), (chain[1], chain[0])):
+        TM = row.bound
+        if not isinstance(TM, nat.Const):
+            continue
+        I = nat.normalize(TM * V(wg.var) + V(row.var))
+        M = nat.normalize(wg.bound * TM, prog.assumptions)
+        desc = _operands(prog, x, y, I, V(col.var), P, M, col.bound, K, store)
+        if desc is not None and desc["value"] == fold[5]:
+            return emit(prog, desc, base_name, temps)
+    return None
+
+
+def emit(prog, desc, base_name, temps):
+    """The gemm_tc kernel and plan for C[M x N] = A[M x K] * B (desc)."""
+    M, N, K = desc["M"], desc["N"], desc["K"]
+    b_mn = desc["b_mn"]
+    a_buf, b_buf, out_buf = desc["a"], desc["b"], desc["out"]
     name = f"{base_name}_gemm"
     r = NatRenderer(prog.clamps)
     bn, stages, write_hi = BN, STAGES, WRITE_HI
@@ -100,7 +286,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
         lines += [
             f"  rise_gemm::{fn}<{r(M)}, {r(N)}, {r(K)}, {PAIR_BN}, {PAIR_STAGES}, "
             f"{'true' if b_mn else 'false'}{(', ' + str(GROUP_M)) if PERSIST and GROUP_M else ''}>"
-            f"({st.target.buf}, {r(N)}, &rs_mapA, &rs_mapB, {args});",
+            f"({out_buf}, {r(N)}, &rs_mapA, &rs_mapB, {args});",
             "}",
         ]
         plan = {
@@ -122,11 +308,11 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
                    + ([f"({py_expr(N)}) % 4 == 0"] if b_mn else []),
             "smem": PAIR_STAGES * 2 * (128 * 32 * 4 + (PAIR_BN // 2) * 32 * 4) + 1024 + 256,
             "extra_args": [
-                {"kind": "tma2d", "buf": a_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(M)],
+                {"kind": "tma2d", "buf": a_buf, "offset": "0", "dims": [py_expr(K), py_expr(M)],
                  "pitch": py_expr(K), "box": [32, 128], "swizzle": 3},
-                ({"kind": "tma2d", "buf": b_ld.buf, "offset": "0", "dims": [py_expr(N), py_expr(K)],
+                ({"kind": "tma2d", "buf": b_buf, "offset": "0", "dims": [py_expr(N), py_expr(K)],
                   "pitch": py_expr(N), "box": [32, 32], "swizzle": 4} if b_mn else
-                 {"kind": "tma2d", "buf": b_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(N)],
+                 {"kind": "tma2d", "buf": b_buf, "offset": "0", "dims": [py_expr(K), py_expr(N)],
                   "pitch": py_expr(K), "box": [32, PAIR_BN // 2], "swizzle": 3}),
                 {"kind": "gemm_full_tiles", "M": py_expr(M), "N": py_expr(N), "K": py_expr(K), "bn": PAIR_BN},
                 *([{"kind": "gemm_units", "M": py_expr(M), "N": py_expr(N), "K": py_expr(K), "bn": PAIR_BN},
@@ -142,7 +328,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
         return "\n".join(lines) + "\n", plan
     lines += [
         f"  rise_gemm::gemm_3xtf32<{r(K)}, {bn}, {stages}, {'true' if write_hi else 'false'}>"
-        f"({st.target.buf}, {r(N)}, &rs_mapA, &rs_mapB);",
+        f"({out_buf}, {r(N)}, &rs_mapA, &rs_mapB);",
         "}",
     ]
     plan = {
@@ -157,9 +343,9 @@ def match(prog, stage, base_name, temps, exact, parallel_rows, fold_shape):
                 f"({py_expr(M)}) * ({py_expr(N)}) * ({py_expr(K)}) > 0"],
         "smem": stages * 2 * (128 * 32 * 4 + bn * 32 * 4) + 1024 + 256,
         "extra_args": [
-            {"kind": "tma2d", "buf": a_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(M)], "pitch": py_expr(K),
+            {"kind": "tma2d", "buf": a_buf, "offset": "0", "dims": [py_expr(K), py_expr(M)], "pitch": py_expr(K),
              "box": [32, 128], "swizzle": 3},
-            {"kind": "tma2d", "buf": b_ld.buf, "offset": "0", "dims": [py_expr(K), py_expr(N)], "pitch": py_expr(K),
+            {"kind": "tma2d", "buf": b_buf, "offset": "0", "dims": [py_expr(K), py_expr(N)], "pitch": py_expr(K),
              "box": [32, bn], "swizzle": 3},
         ],
     }

@@ -15,6 +15,8 @@ EXPECTED_TEMPLATE = {
     "gemv_opt": "rowfold",
     "conv": "stencil2d",
     "nbody": "allpairs",
+    "sgemm": "gemm_tc",
+    "sgemm_tiled": "gemm_tc",
 }
 
 
@@ -217,3 +219,30 @@ def test_layout_templates_selected_and_compile(name, source, nats, kind):
     names = [f"{s['name']}<{targs}>" for st in code.plan["stages"] for s in (st, st.get("fallback")) if s]
     cubin, lowered = runtime.compile_cubin(code.text, names, ["--fmad=false"])
     assert cubin[:4] == b"\x7fELF" and len(lowered) == len(names)
+
+
+def test_tiled_sgemm_is_recognised_as_the_contraction():
+    """C4's tiled lowering (split / toMem(Local) / transpose / K tiles under
+    mapWorkGroup / mapLocal) is claimed by gemm_tc with the flat operands:
+    A K-major through the Local staging, B MN-major through the transpose."""
+    st = _code("sgemm_tiled").plan["stages"][0]
+    assert st["kind"] == "gemm_tc" and (st["M"], st["N"], st["K"]) == ("n", "m", "k")
+    assert st["b_major"] == "mn" and st["fallback"]["kind"] == "workgroup"
+    bufs = {e["buf"] for e in st["extra_args"] if e["kind"] == "tma2d"}
+    assert bufs == {"A", "B"}
+    # order-preserving emission keeps the program's own order: no tensor cores
+    code = emit_cuda(programs.compile_config("sgemm_tiled").unit, reassociate=False)
+    assert [s["kind"] for s in code.plan["stages"]] == ["workgroup"]
+
+
+@pytest.mark.parametrize("edit", [
+    ("acc + fst(p) * snd(p)", "acc + fst(p) * fst(p)"),     # not a product of A and B
+    ("acc + fst(p) * snd(p)", "acc + fst(p) - snd(p)"),     # not a product
+    ("(fun(acc, v => acc + v))(0.0f)", "(fun(acc, v => acc + v))(1.0f)"),  # non-zero init
+    ("v * 1.0f", "v * 2.0f"),                                # the staging is not a copy
+])
+def test_tiled_sgemm_near_misses_stay_generic(edit):
+    src = programs.SGEMM_TILED.replace(*edit)
+    assert src != programs.SGEMM_TILED
+    c = compile_program(src, None, name="sgemmTiled", assumptions=programs.sgemm_tiled_assumptions())
+    assert [s["kind"] for s in emit_cuda(c.unit).plan["stages"]] == ["workgroup"]

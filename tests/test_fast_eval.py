@@ -74,13 +74,13 @@ CONFIG_SIZES = {
     "conv": {"n": 6, "m": 7},
     "sgemm": {"n": 4, "m": 5, "k": 6},
     "nbody": {"n": 8},
+    "sgemm_tiled": {"n": 4, "m": 5, "k": 64},
 }
 
 
 @pytest.mark.parametrize("key", sorted(CONFIG_SIZES))
 def test_config_programs_bit_identical(key):
-    cfg = programs.CONFIGS[key]
-    c = compile_program(cfg["source"], cfg["strategy"], name=cfg["name"])
+    c = programs.compile_config(key)
     nats = CONFIG_SIZES[key]
     rng = random.Random(len(key))
     for prog in (c.source_typed, c.lowered):  # before and after the strategy

@@ -449,3 +449,43 @@ def test_sgemm_single_cta_variant_within_bound(gpu):
     )
     root = str(__import__("pathlib").Path(__file__).resolve().parent.parent)
     subprocess.run([sys.executable, "-c", code], check=True, cwd=root, env=dict(os.environ, RISE_GEMM_2SM="0"))
+
+
+def test_sgemm_tiled_generic_kernel_bit_exact_with_its_program(gpu):
+    """The tiled C4 program's own order (Local-staged A rows, per-K-tile
+    partial sums, then their sum) on the generic GPU kernel: bit-identical
+    to the vectorised functional oracle of the same program."""
+    import fast_eval
+
+    c = programs.compile_config("sgemm_tiled")
+    code = emit_cuda(c.unit, idioms=False)
+    assert [s["kind"] for s in code.plan["stages"]] == ["workgroup"]
+    n, m, k = 34, 300, 256
+    A = oracle.rng_inputs(4, n, k)
+    B = oracle.rng_inputs(24, k, m)
+    got = run_cuda(code, c.unit, {"n": n, "m": m, "k": k}, [A, B], as_numpy=True).reshape(n, m)
+    want = fast_eval.to_numpy(fast_eval.eval_program(c.source_typed, {"n": n, "m": m, "k": k}, [A, B]))
+    np.testing.assert_array_equal(got.view(np.uint32), np.asarray(want, np.float32).reshape(n, m).view(np.uint32))
+
+
+@pytest.mark.parametrize("n,m,k", [(256, 512, 512), (4096, 4096, 4096)])
+def test_sgemm_tiled_program_on_the_tensor_cores(gpu, n, m, k):
+    """C4 as BASELINE.json names it (programs.SGEMM_TILED) runs on gemm_tc:
+    every element within 2 k u (|A||B|) of fp64, and within the sum of the
+    two bounds of the reference's own emitted C (oracle/_ref sgemmBt, its
+    sequential k fold) on the same inputs."""
+    c = programs.compile_config("sgemm_tiled")
+    code = emit_cuda(c.unit)
+    assert code.plan["stages"][0]["kind"] == "gemm_tc"
+    A = oracle.rng_inputs(4, n, k)
+    B = oracle.rng_inputs(24, k, m)
+    got = run_cuda(code, c.unit, {"n": n, "m": m, "k": k}, [A, B], as_numpy=True).reshape(n, m)
+    Bt = np.ascontiguousarray(B.T)
+    C64, absC = _gemm_f64(A, Bt)
+    bound = oracle.gemm_bound(k, absC)
+    err = np.abs(got - C64)
+    assert np.all(err <= bound), float(np.max(err / (absC * oracle.U * k)))
+    assert float(np.max(err / absC)) < 1e-5
+    if oracle.ref_lib() is not None:
+        ref = oracle.ref_sgemm_bt(A, Bt)
+        assert np.all(np.abs(got - ref) <= 2 * bound)

@@ -7,7 +7,7 @@ produces — over one batch of synthetic, seeded input already resident in
 HBM.  The headline is BASELINE.json configs[1], gemv fp32 8192x8192
 (`mv.rise` + the toMapGlobal strategy); the same JSON line carries
 `per_config`, every BASELINE config (C1 dot, C2 gemv, C3 conv, C4 sgemm,
-C5 nbody) measured the same way, each with its roofline, its full-size CPU
+C5 nbody; C4 as the tiled program BASELINE names) measured the same way, each with its roofline, its full-size CPU
 baseline (the reference's emitted C/OpenMP on this host) and its e2e figure.
 
 `--gpus N` runs N ranks, one per GPU: without torchrun's environment the
@@ -53,7 +53,8 @@ ROTATE_BYTES = 512 << 20  # input sets used round robin cover >= 4x L2
 FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # derived, BASELINE.md §2
 TF32_DENSE_TFLOPS = 1100.0  # B200_PROFILING.md fallback (MEASURED_PEAKS has no TF32 entry)
 HEADLINE = "gemv"
-PER_CONFIG = ("dot", "gemv", "conv", "sgemm", "nbody")  # BASELINE.json configs[0..4]
+# BASELINE.json configs[0..4]; C4 is the tiled split / transpose / toMem(Local) lowering it names
+PER_CONFIG = ("dot", "gemv", "conv", "sgemm_tiled", "nbody")
 METRIC = "per-benchmark GFLOP/s or GB/s vs B200 roofline at 1/2/4/8 GPUs vs CPU ref"
 
 
@@ -378,7 +379,7 @@ class SgemmNN(Sgemm):
         return super().cpu_fn([A, np.ascontiguousarray(B.T)])  # the reference C takes Bt
 
 
-class SgemmTiled(Sgemm):
+class SgemmTiled(SgemmNN):
     key = "sgemm_tiled"
     program = ("the tiled C4 program (programs.SGEMM_TILED: split / transpose / toMem(Local) under mapWorkGroup / "
                "mapLocal, K tiles) -> the tcgen05 3xTF32 template")

@@ -41,7 +41,7 @@ def test_bench_prints_one_contract_line_with_every_config(gpu):
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
     _check_entry(d)
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
-    assert set(d["per_config"]) == {"dot", "gemv", "conv", "sgemm", "nbody"}
+    assert set(d["per_config"]) == {"dot", "gemv", "conv", "sgemm_tiled", "nbody"}
     for key, entry in d["per_config"].items():
         _check_entry(entry)
         assert entry["config"]["workload"].startswith(key)
@@ -52,7 +52,7 @@ def test_bench_gpus_2_runs_two_ranks(gpu):
     env = dict(os.environ, RISE_BENCH_SHARED_GPU="1", RISE_DIST_BACKEND="gloo")
     env.pop("WORLD_SIZE", None)
     out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
-                          "--configs", "dot,conv,sgemm,nbody"], cwd=ROOT, capture_output=True, text=True,
+                          "--configs", "dot,conv,sgemm_tiled,nbody"], cwd=ROOT, capture_output=True, text=True,
                          timeout=900, env=env)
     d = _line(out)
     assert d["n_gpus"] == 2 and d["scaling"] == "strong"
@@ -61,7 +61,7 @@ def test_bench_gpus_2_runs_two_ranks(gpu):
     assert "with_collective" in d
     for key, entry in d["per_config"].items():
         _check_entry(entry)
-    assert d["per_config"]["sgemm"]["impl_detail"]["rank_sizes"]["n"] == 2048
+    assert d["per_config"]["sgemm_tiled"]["impl_detail"]["rank_sizes"]["n"] == 2048
     assert d["per_config"]["dot"]["impl_detail"]["rank_sizes"]["n"] == 1 << 23
 
 

@@ -125,15 +125,45 @@ SGEMM_TILED = """\
 def sgemmTiled = depFun((n: Nat, m: Nat, k: Nat) =>
   fun(A: Array[n, Array[k, f32]] => fun(B: Array[k, Array[m, f32]] =>
     A |> split(2) |> mapWorkGroup(fun(aBlock =>
-      aBlock |> mapSeq(fun(arow => arow |> mapLocal(fun(v => v * 1.0f)))) |> toMem(Local) |> fun(aLocal =>
-        aLocal |> mapSeq(fun(arow =>
+      aBlock |> mapSeq(mapLocal(fun(v => v * 1.0f))) |> toMem(Local)
+        |> mapSeq(fun(arow =>
           transpose(B) |> mapLocal(fun(bcol =>
             zip(arow)(bcol) |> split(32)
               |> mapSeq(fun(tile => tile |> reduceSeq(Private)(fun(acc, p => acc + fst(p) * snd(p)))(0.0f)))
               |> toMem(Private)
-              |> reduceSeq(Private)(fun(acc, v => acc + v))(0.0f) )) )) ) )) |> join )))
+              |> reduceSeq(Private)(fun(acc, v => acc + v))(0.0f) )) )) )) |> join )))
 """
 SGEMM_TILE_ROWS, SGEMM_TILE_K = 2, 32
+
+# the high-level programs the GPU strategies (gpu_rules.*_STRATEGY) lower to
+# CONV, SGEMM_TILED and NBODY (SURVEY.md §8 f 3)
+CONV_HIGH = """\
+def conv = depFun((n: Nat, m: Nat) => fun(img: Array[n, Array[m, f32]] => fun(w: Array[3, Array[3, f32]] =>
+  img |> padClamp2D(1)(1) |> slide2D(3)(1) |> map(map(fun(win =>
+    zip(win)(w)
+      |> map(fun(rw => zip(fst(rw))(snd(rw)) |> map(fun(p => fst(p) * snd(p))) |> reduce(add)(0.0f)))
+      |> reduce(add)(0.0f) ))) )))
+"""
+
+SGEMM_HIGH = """\
+def sgemmTiled = depFun((n: Nat, m: Nat, k: Nat) =>
+  fun(A: Array[n, Array[k, f32]] => fun(B: Array[k, Array[m, f32]] =>
+    A |> map(fun(arow => transpose(B) |> map(fun(bcol =>
+      zip(arow)(bcol) |> map(fun(p => fst(p) * snd(p))) |> reduce(add)(0.0f) )))) )))
+"""
+
+NBODY_HIGH = """\
+def nbody = depFun((n: Nat) =>
+  fun(pos: Array[n, Array[3, f32]] => fun(vel: Array[n, Array[3, f32]] => fun(mass: Array[n, f32] =>
+    zip(pos)(vel) |> map(fun(pv =>
+      zip(transpose(pos))(zip(fst(pv))(snd(pv))) |> map(fun(col =>
+        snd(snd(col)) + 0.01f *
+          (zip(fst(col))(zip(pos)(mass)) |> map(fun(q =>
+             (fst(q) - fst(snd(col))) *
+               (snd(snd(q)) *
+                 ((zip(fst(snd(q)))(fst(pv)) |> map(fun(d => (fst(d) - snd(d)) * (fst(d) - snd(d)))) |> reduce(add)(0.01f))
+                   |> fun(r2 => rsqrt(r2) * rsqrt(r2) * rsqrt(r2)))) )) |> reduce(add)(0.0f)) )) )) ))))
+"""
 
 
 def sgemm_tiled_assumptions():

@@ -246,3 +246,29 @@ def test_tiled_sgemm_near_misses_stay_generic(edit):
     assert src != programs.SGEMM_TILED
     c = compile_program(src, None, name="sgemmTiled", assumptions=programs.sgemm_tiled_assumptions())
     assert [s["kind"] for s in emit_cuda(c.unit).plan["stages"]] == ["workgroup"]
+
+
+@pytest.mark.parametrize("key,high,strategy_name", [
+    ("conv", "CONV_HIGH", "CONV_STRATEGY"),
+    ("sgemm_tiled", "SGEMM_HIGH", "SGEMM_TILED_STRATEGY"),
+    ("nbody", "NBODY_HIGH", "NBODY_STRATEGY"),
+])
+def test_gpu_strategies_derive_the_hand_lowered_programs(key, high, strategy_name):
+    """SURVEY.md §8 f 3: the high-level map/reduce programs, rewritten by the
+    .elv strategies (reference rules + gpu_rules' splitReduce(c, a),
+    insertToMemReduce, stageToMem), emit byte-identical sm100a text to the
+    hand-lowered programs the templates take — with the same recorded
+    divisibility assumptions."""
+    from paper_2201_03611_b200 import gpu_rules
+
+    derived = compile_program(getattr(programs, high), getattr(gpu_rules, strategy_name))
+    hand = programs.compile_config(key)
+    assert emit_cuda(derived.unit).text == emit_cuda(hand.unit).text
+    assert set(derived.assumptions) == set(hand.assumptions)
+
+
+def test_strategy_rules_are_registered_for_strategy_files():
+    from paper_2201_03611_b200._ref import rules
+
+    for name in ("splitReduce", "splitMap", "insertToMemReduce", "stageToMem"):
+        assert name in rules.RULES and name in rules.RULE_PARAMS

@@ -130,3 +130,40 @@ def test_large_sizes_are_fast():
     for v in chunks:
         total = np.float32(total + v)
     assert out.view(np.uint32) == np.asarray(total).view(np.uint32)
+
+
+@pytest.mark.parametrize("high,strategy_name,nats", [
+    ("CONV_HIGH", "CONV_STRATEGY", {"n": 6, "m": 7}),
+    ("NBODY_HIGH", "NBODY_STRATEGY", {"n": 8}),
+])
+def test_gpu_strategies_preserve_the_program_bit_for_bit(high, strategy_name, nats):
+    """The conv and nbody strategies only fuse and lower (no reassociation):
+    the rewritten program evaluates bit-identically to the high-level one."""
+    c = compile_program(getattr(programs, high), getattr(gpu_rules, strategy_name))
+    rng = random.Random(11)
+    for _ in range(3):
+        inputs = _inputs(c.source_typed, nats, rng)
+        _same(fast_eval.eval_program(c.lowered, nats, inputs), interpreter.eval_program(c.source_typed, nats, inputs))
+
+
+def test_sgemm_tiled_strategy_reassociates_k_into_tiles_only():
+    """The sgemm strategy's one reassociation is the K fold in tiles of 32:
+    the rewritten program equals sum over tiles of each tile's left fold."""
+    c = compile_program(programs.SGEMM_HIGH, gpu_rules.SGEMM_TILED_STRATEGY)
+    rng = np.random.default_rng(5)
+    n, m, k = 4, 3, 96
+    A = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    B = rng.uniform(-1, 1, (k, m)).astype(np.float32)
+    got = np.asarray(fast_eval.to_numpy(fast_eval.eval_program(c.lowered, {"n": n, "m": m, "k": k}, [A, B])),
+                     np.float32).reshape(n, m)
+    want = np.zeros((n, m), np.float32)
+    for i in range(n):
+        for j in range(m):
+            total = np.float32(0)
+            for t in range(k // 32):
+                part = np.float32(0)
+                for p in range(32 * t, 32 * t + 32):
+                    part = np.float32(part + np.float32(A[i, p] * B[p, j]))
+                total = np.float32(total + part)
+            want[i, j] = total
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))

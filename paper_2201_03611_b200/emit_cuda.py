@@ -42,7 +42,7 @@ import warnings
 from dataclasses import dataclass, field
 
 from . import lir
-from ._ref import errors, nat
+from ._ref import codegen, errors, nat
 
 EmitError = errors.EmitError
 
@@ -55,20 +55,28 @@ DEFAULT_BLOCK = 256
 # rendering of sizes / indices
 
 
-def _strip_neg(t):
-    if isinstance(t, nat.Const) and t.value < 0:
-        return True, nat.Const(-t.value)
-    if isinstance(t, nat.Product) and t.factors and isinstance(t.factors[0], nat.Const) and t.factors[0].value < 0:
-        c = -t.factors[0].value
-        rest = t.factors[1:]
-        if c == 1:
-            return True, rest[0] if len(rest) == 1 else nat.Product(rest)
-        return True, nat.Product((nat.Const(c),) + rest)
-    return False, t
+def _has_pow(n) -> bool:
+    if isinstance(n, nat.Pow):
+        return True
+    if isinstance(n, nat.Sum):
+        return any(_has_pow(t) for t in n.terms)
+    if isinstance(n, nat.Product):
+        return any(_has_pow(f) for f in n.factors)
+    if isinstance(n, (nat.Div, nat.Mod)):
+        return _has_pow(n.num) or _has_pow(n.den)
+    return False
 
 
 class NatRenderer:
-    """Nat -> C (or Python) integer expression text."""
+    """Nat -> C (or Python) integer expression text.
+
+    Plain C index text is the reference emitter's own rendering
+    (codegen._render, codegen.py:80-110: the same normal form, precedence
+    and negation handling), so emitted indices read exactly like the
+    reference's.  This class adds what the reference has no notion of:
+    clamped (padClamp) index atoms -> rs_clamp(...), renamed variables,
+    `ipow` spelled rs_ipow, and the Python spelling (// and **) of launch
+    expressions evaluated by the planner."""
 
     def __init__(self, clamps=None, py=False, names=None):
         self.clamps = clamps or {}
@@ -79,6 +87,11 @@ class NatRenderer:
         return self.render(n, prec)
 
     def render(self, n, prec=0):
+        if not self.py and not _has_pow(n) and not (nat.free_vars(n) & (set(self.clamps) | set(self.names))):
+            return codegen._render(n, codegen._State(TARGET, ()), prec)
+        return self._render(n, prec)
+
+    def _render(self, n, prec=0):
         if isinstance(n, nat.Const):
             return str(n.value) if n.value >= 0 else f"(-{-n.value})"
         if isinstance(n, nat.Var):
@@ -90,7 +103,7 @@ class NatRenderer:
             return self.names.get(n.name, n.name)
         if isinstance(n, nat.Sum):
             parts = []
-            terms = [_strip_neg(t) for t in n.terms]
+            terms = [nat._strip_negation(t) for t in n.terms]
             terms = [t for t in terms if not t[0]] + [t for t in terms if t[0]]
             for k, (neg, body) in enumerate(terms):
                 s = self.render(body, 1)

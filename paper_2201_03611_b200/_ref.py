@@ -28,6 +28,7 @@ except ImportError:  # pragma: no cover
 
 from risec import (  # noqa: E402,F401
     cexec,
+    cli,
     codegen,
     dpia,
     errors,

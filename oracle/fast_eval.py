@@ -253,9 +253,9 @@ def exec_prim(name, deps, args, nat_env, depth):
     if name in ("fst", "snd"):
         (p,) = args
         return p.a if name == "fst" else p.b
-    if name == "split":
+    if name in ("split", "asVector"):  # asVector(w) is split(w) as a value (extension.py)
         return on_axes(args[0], lambda a, nb: _split(a, nb, deps[0]))
-    if name == "join":
+    if name in ("join", "asScalar"):
         return on_axes(args[0], _join)
     if name == "transpose":
         return on_axes(args[0], _transpose)

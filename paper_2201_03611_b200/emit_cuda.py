@@ -276,10 +276,31 @@ class CudaCode:
     program: lir.Program = field(repr=False, default=None)
 
 
-class GenericKernel:
-    """One stage -> one kernel with the generic GPU mapping."""
+def _map_value(e, load_fn, sub):
+    """Rebuild a value with `load_fn` applied to its loads and the index
+    substitution `sub` applied to every index."""
+    if isinstance(e, lir.Load):
+        return load_fn(e)
+    if isinstance(e, lir.IndexVal):
+        return lir.IndexVal(nat.normalize(nat.substitute(e.n, sub)), e.ctype)
+    if isinstance(e, lir.Bin):
+        return lir.Bin(e.op, _map_value(e.a, load_fn, sub), _map_value(e.b, load_fn, sub), e.ctype)
+    if isinstance(e, lir.Un):
+        return lir.Un(e.fn, _map_value(e.a, load_fn, sub), e.ctype)
+    return e
 
-    def __init__(self, prog: lir.Program, stage: Stage, name: str, temps, exact=True):
+
+class GenericKernel:
+    """One stage -> one kernel with the generic GPU mapping.
+
+    `vectorize=True`: a constant loop over the w = 2 / 4 lanes of a vector
+    (asVector / asScalar views: lir.Load.vec / Store.vec) reads its lanes
+    with one float2 / float4 load and writes them with one vector store —
+    Shine's vector types as float4 pointers.  The
+    caller keeps the scalar kernel as the fallback for buffers that are not
+    16-byte aligned."""
+
+    def __init__(self, prog: lir.Program, stage: Stage, name: str, temps, exact=True, vectorize=False):
         self.prog = prog
         self.stage = stage
         self.name = name
@@ -289,6 +310,70 @@ class GenericKernel:
         self.shared_decls = []
         self.shared_names = set()
         self.smem_bytes = []  # py size expressions of static shared arrays
+        self.vectorize = vectorize
+        self.vector_accesses = 0  # vector loads + stores emitted
+
+    def _vector_for(self, s, ind):
+        """The lanes loop of a vector: one vector load per (buffer, base),
+        the w lanes unrolled, one vector store per written vector; None when
+        the loop does not qualify."""
+        w, v = s.bound.value, s.var
+        body = s.body.stmts if isinstance(s.body, lir.Seq) else [s.body]
+        if not all(isinstance(x, lir.Assign) for x in body):
+            return None
+        written = {x.target.buf for x in body if isinstance(x.target, lir.Store)}
+        read = {ld.buf for x in body for ld in lir.expr_loads(x.value)}
+
+        def base_of(ix):
+            return nat.normalize(ix - nat.Var(v))
+
+        loads, stores = {}, {}
+        for x in body:
+            for ld in lir.expr_loads(x.value):
+                if ld.vec == (w, v) and ld.ctype == "float" and ld.buf not in written:
+                    loads.setdefault((ld.buf, base_of(ld.index)), f"rs_vl{len(loads)}")
+        for x in body:
+            t = x.target
+            if isinstance(t, lir.Store) and t.vec == (w, v) and t.ctype == "float" and t.buf not in read:
+                key = (t.buf, base_of(t.index))
+                if key in stores:
+                    return None  # a lane written twice: keep the scalar order
+                stores[key] = f"rs_vs{len(stores)}"
+        if not loads and not stores:
+            return None
+        vt = "float4" if w == 4 else "float2"
+        p = "  " * ind
+        out = [f"{p}{{  // the {w} lanes of a vector: {vt} accesses"]
+        for (buf, base), nm in loads.items():
+            out.append(f"{p}  const {vt} {nm} = *reinterpret_cast<const {vt}*>({buf} + ({self.nat(base)}));")
+        for (buf, base), nm in stores.items():
+            out.append(f"{p}  {vt} {nm};")
+        for k in range(w):
+            comp = "xyzw"[k]
+            sub = {v: nat.Const(k)}
+
+            def load_fn(ld, comp=comp, sub=sub):
+                key = (ld.buf, base_of(ld.index))
+                if ld.vec == (w, v) and key in loads:
+                    return lir.ScalarRef(f"{loads[key]}.{comp}", ld.ctype)
+                return lir.Load(ld.buf, nat.normalize(nat.substitute(ld.index, sub)), ld.ctype)
+
+            lane = []
+            for x in body:
+                t = x.target
+                if isinstance(t, lir.Store):
+                    key = (t.buf, base_of(t.index))
+                    if t.vec == (w, v) and key in stores:
+                        t = lir.ScalarRef(f"{stores[key]}.{comp}", t.ctype)
+                    else:
+                        t = lir.Store(t.buf, nat.normalize(nat.substitute(t.index, sub)), t.ctype)
+                lane.append(lir.Assign(t, _map_value(x.value, load_fn, sub)))
+            out += self.thread(lir.Seq(lane), ind + 1)
+        for (buf, base), nm in stores.items():
+            out.append(f"{p}  *reinterpret_cast<{vt}*>({buf} + ({self.nat(base)})) = {nm};")
+        out.append(f"{p}}}")
+        self.vector_accesses += len(loads) + len(stores)
+        return out
 
     # helpers -------------------------------------------------------------
     def _size_c(self, dims):
@@ -327,6 +412,11 @@ class GenericKernel:
             else:
                 decl = f"{p}{s.ctype} {s.name};"
             return [decl] + self.thread(s.body, ind)
+        if (self.vectorize and isinstance(s, lir.For) and isinstance(s.bound, nat.Const)
+                and s.bound.value in (2, 4)):
+            out = self._vector_for(s, ind)
+            if out is not None:
+                return out
         if isinstance(s, (lir.For, lir.ParFor)):
             head = f"{p}for (int {s.var} = 0; {s.var} < {self.nat(s.bound)}; {s.var} += 1) {{"
             pre = []
@@ -493,6 +583,40 @@ def arg_names(prog: lir.Program, temps):
 # whole units
 
 
+def _stage_buffers(stmt) -> set:
+    out = set()
+    for t, v in lir.stmt_exprs(stmt):
+        if isinstance(t, lir.Store):
+            out.add(t.buf)
+        out.update(ld.buf for ld in lir.expr_loads(v))
+    return out
+
+
+def reuse_slots(stages, temps) -> dict:
+    """Memory reuse of the Global temporaries (toMem(Global) between kernel
+    stages): a temporary lives from the first to the last stage that touches
+    it, and temporaries whose lives do not overlap share one allocation
+    (greedy first fit in order of first use).  -> {temp name: slot index}."""
+    life = {}
+    for st in stages:
+        for b in _stage_buffers(st.stmt):
+            lo, hi = life.get(b, (st.index, st.index))
+            life[b] = (min(lo, st.index), max(hi, st.index))
+    slots = []  # per slot: the last stage index of its current occupant
+    out = {}
+    for t in sorted(temps, key=lambda t: life.get(t.name, (-1, -1))):
+        lo, hi = life.get(t.name, (-1, -1))
+        for k, end in enumerate(slots):
+            if end < lo:
+                slots[k] = hi
+                out[t.name] = k
+                break
+        else:
+            out[t.name] = len(slots)
+            slots.append(hi)
+    return out
+
+
 class SingleBlockStage(UserWarning):
     """A kernel stage that runs in one block / one thread on the GPU."""
 
@@ -541,7 +665,15 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, pee
                 if inc not in includes:
                     includes.append(inc)
             entry = dict(match.plan, fallback=generic.plan)
-        elif st.kind in ("block", "serial"):
+        else:
+            # vector views (asVector / asScalar): the same kernel with float2 /
+            # float4 accesses, the scalar kernel kept as its fallback
+            vec = GenericKernel(prog, st, base + "_vec", temps, exact, vectorize=True)
+            vtext = vec.emit()
+            if vec.vector_accesses:
+                kernels.append(vtext.text)
+                entry = dict(vtext.plan, fallback=generic.plan, vector=True)
+        if match is None and st.kind in ("block", "serial"):
             # a top-level sequential loop (or fold) no template claims runs in ONE
             # block (one thread for "serial"): correct, but a performance cliff
             entry["single_block"] = True
@@ -566,6 +698,7 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, pee
         kernels = [_pdl_insert(kt, names(plan_stages[1:]), "griddepcontrol.wait;",
                                "PDL: the previous stage is done")
                    for kt in kernels]
+    slot_of = reuse_slots(stages, temps)
     plan = {
         "version": 1,
         "target": TARGET,
@@ -575,7 +708,8 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, pee
         "output": {"name": prog.output.name, "ctype": prog.output.ctype,
                    "size": py_expr(_prod(prog.output.dims)), "deref": prog.output.deref},
         "inputs": [_input_plan(n, b) for n, b in prog.inputs],
-        "temps": [{"name": t.name, "ctype": t.ctype, "size": py_expr(_prod(t.dims))} for t in temps],
+        "temps": [{"name": t.name, "ctype": t.ctype, "size": py_expr(_prod(t.dims)), "slot": slot_of[t.name]}
+                  for t in temps],
         "stages": plan_stages,
         "exact": exact,
         "reassociate": reassociate,

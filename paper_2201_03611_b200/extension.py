@@ -39,10 +39,17 @@ them in the sense of SURVEY.md §8 c; these definitions are the spec):
   rounded to binary32 (the GPU evaluates it with the MUFU reciprocal square
   root, so programs using it are compared under a tolerance).
 * `toGlobal/toLocal/toPrivate` = `toMem(Global/Local/Private)`.
+* `asVector(w)`: Array[w*q, t] -> Array[q, Array[w, t]] and `asScalar`:
+  Array[a, Array[b, t]] -> Array[a*b, t] — Shine's vector views
+  (PAPER.md:1047-1051): as values they are split(w) / join; as memory
+  accesses they promise that the w elements of a vector are contiguous
+  and w-aligned, so the sm100a emitter reads / writes them as one float2 /
+  float4 (emit_cuda.GenericKernel, `vectorize`).
 """
 
 from __future__ import annotations
 
+import dataclasses
 import re
 
 import numpy as np
@@ -66,6 +73,8 @@ SCHEMES = {
     "toGlobal": "{t: DataType} -> t -> t",
     "toLocal": "{t: DataType} -> t -> t",
     "toPrivate": "{t: DataType} -> t -> t",
+    "asVector": "(w: Nat) -> {q: Nat} -> {t: DataType} -> Array[w * q, t] -> Array[q, Array[w, t]]",
+    "asScalar": "{a: Nat} -> {b: Nat} -> {t: DataType} -> Array[a, Array[b, t]] -> Array[a * b, t]",
 }
 
 # ---------------------------------------------------------------------------
@@ -86,7 +95,14 @@ SIGNATURE_TEXT = {
     "toPrivate": "(t: DataType, x: Exp[t,Wr]): Exp[t,Rd]",
     # imperative: the acceptor view written through by accT(transpose)
     "transposeAcc": "(n: Nat, m: Nat, t: DataType, array: Acc[Array[m,Array[n,t]]]): Acc[Array[n,Array[m,t]]]",
+    # vector views: split / join with the same index maps (dpia.py:240-241, 259-260)
+    "asVector": "(n: Nat, m: Nat, t: DataType, w: ReadWrite, x: Exp[Array[n*m,t],w]): Exp[Array[m,Array[n,t]],w]",
+    "asScalar": "(n: Nat, m: Nat, t: DataType, w: ReadWrite, x: Exp[Array[n,Array[m,t]],w]): Exp[Array[n*m,t],w]",
+    "asVectorAcc": "(n: Nat, m: Nat, t: DataType, array: Acc[Array[m,Array[n,t]]]): Acc[Array[n*m,t]]",
+    "asScalarAcc": "(n: Nat, m: Nat, t: DataType, array: Acc[Array[n*m,t]]): Acc[Array[n,Array[m,t]]]",
 }
+# each vector view and acceptor behaves as its split / join counterpart
+VECTOR_AS = {"asVector": "split", "asScalar": "join", "asVectorAcc": "splitAcc", "asScalarAcc": "joinAcc"}
 
 VIEW_TAGS = ("transpose", "slide", "padClamp", "padClamp2D", "slide2D")
 BINARY_TAGS = ("div",)
@@ -152,6 +168,8 @@ def _install_lowering():
             return (out, dpia.RWVar(lowering._fresh_rw(ctx)))
         if tag in TO_MEM_ALIASES:
             return (out,)
+        if tag in ("asVector", "asScalar"):
+            return base_targs(VECTOR_AS[tag], vt, deps, ctx)
         return base_targs(tag, vt, deps, ctx)
 
     lowering._targs_for = targs_for
@@ -192,8 +210,23 @@ def _install_lowering():
 
         return handler
 
-    for tag in VIEW_TAGS:
+    def acc_vector(acc_tag):
+        # accT(asVector(x)) / accT(asScalar(x)): x written through the dual
+        # acceptor (lowering.py:404-417 with the vector tags)
+        def handler(ctx, expr, output):
+            n, m, t, _w = expr.type_args
+            (arr,) = expr.args
+            shape = (lowering.ArrayType(nat.normalize(n * m), t) if acc_tag == "asVectorAcc"
+                     else lowering.ArrayType(n, lowering.ArrayType(m, t)))
+            view = dpia.ImpPrim(acc_tag, (n, m, t), (output,), dpia.AccType(shape))
+            return lowering.acc_t(ctx, arr, view)
+
+        return handler
+
+    for tag in VIEW_TAGS + ("asVector", "asScalar"):
         lowering._CON_CASES[tag] = lowering._con_passthrough
+    lowering._ACC_CASES["asVector"] = acc_vector("asVectorAcc")
+    lowering._ACC_CASES["asScalar"] = acc_vector("asScalarAcc")
     lowering._ACC_CASES["transpose"] = acc_transpose
     for tag in BINARY_TAGS:
         lowering._ACC_CASES[tag] = lowering._acc_binop
@@ -265,7 +298,8 @@ def any_abs(a):
 
 def _install_interpreter():
     arity = {"transpose": 1, "slide": 1, "padClamp": 1, "padClamp2D": 1, "slide2D": 1,
-             "div": 2, "sqrt": 1, "rsqrt": 1, "abs": 1, "toGlobal": 1, "toLocal": 1, "toPrivate": 1}
+             "div": 2, "sqrt": 1, "rsqrt": 1, "abs": 1, "toGlobal": 1, "toLocal": 1, "toPrivate": 1,
+             "asVector": 1, "asScalar": 1}
     interpreter._PRIM_ARITY.update(arity)
     base_exec = interpreter._exec_prim
 
@@ -294,6 +328,8 @@ def _install_interpreter():
             return any_abs(args[0])
         if name in TO_MEM_ALIASES:
             return args[0]
+        if name in ("asVector", "asScalar"):
+            return base_exec(VECTOR_AS[name], deps, args, nat_env)
         return base_exec(name, deps, args, nat_env)
 
     interpreter._exec_prim = exec_prim
@@ -319,6 +355,8 @@ def _install_interpreter():
             return f32_rsqrt(ev(p.args[0], env, store, nat_env))
         if tag == "abs":
             return any_abs(ev(p.args[0], env, store, nat_env))
+        if tag in ("asVector", "asScalar"):
+            return base_fun(dataclasses.replace(p, tag=VECTOR_AS[tag]), env, store, nat_env)
         return base_fun(p, env, store, nat_env)
 
     interpreter._eval_fun_prim = eval_fun_prim
@@ -329,6 +367,8 @@ def _install_interpreter():
         if isinstance(p, dpia.ImpPrim) and p.tag == "transposeAcc":
             base = eval_acc_phrase(p.args[0], env, store, nat_env).resolve(store)
             return base.via(lambda tail: (tail[1], tail[0]) + tail[2:])
+        if isinstance(p, dpia.ImpPrim) and p.tag in ("asVectorAcc", "asScalarAcc"):
+            return base_acc(dataclasses.replace(p, tag=VECTOR_AS[p.tag]), env, store, nat_env)
         return base_acc(p, env, store, nat_env)
 
     interpreter.eval_acc_phrase = eval_acc_phrase
@@ -379,6 +419,8 @@ def _install_c_emitter():
                 i, j, *rest = pending
                 return emit_exp(x, env, state, (_clamp_nat(i - l, n, state), _clamp_nat(j - l, m, state), *rest),
                                 projs)
+        if isinstance(p, dpia.FunPrim) and p.tag in ("asVector", "asScalar"):
+            return emit_exp(dataclasses.replace(p, tag=VECTOR_AS[p.tag]), env, state, pending, projs)
         if isinstance(p, dpia.FunPrim) and p.tag in BINARY_TAGS + UNARY_TAGS:
             if pending or projs:
                 raise errors.EmitError("indexed arithmetic value")
@@ -397,6 +439,8 @@ def _install_c_emitter():
         if isinstance(p, dpia.ImpPrim) and p.tag == "transposeAcc":
             i, j, *rest = pending
             return emit_acc(p.args[0], env, state, (j, i, *rest))
+        if isinstance(p, dpia.ImpPrim) and p.tag in ("asVectorAcc", "asScalarAcc"):
+            return emit_acc(dataclasses.replace(p, tag=VECTOR_AS[p.tag]), env, state, pending)
         return base_acc(p, env, state, pending)
 
     def emit(unit, target):

@@ -51,6 +51,7 @@ class Load:
     index: object  # nat.Nat (flat)
     ctype: str
     indices: tuple = ()  # per-dimension indices before flattening (analysis only)
+    vec: tuple = ()  # (w, lane var): read through asVector(w), index = base + lane, w | base
 
 
 @dataclass(frozen=True)
@@ -83,6 +84,7 @@ class Store:
     buf: str
     index: object  # nat.Nat (flat)
     ctype: str
+    vec: tuple = ()  # (w, lane var): written through asScalar of w-vectors, index = base + lane, w | base
 
 
 @dataclass
@@ -237,6 +239,7 @@ class Builder:
         self.names: dict = {}
         self._used = set()
         self._clamp_cache: dict = {}
+        self._vec = []  # innermost asVector / asScalarAcc being resolved: (w, lane index)
 
     # names ---------------------------------------------------------------
     def cname(self, name: str) -> str:
@@ -253,6 +256,36 @@ class Builder:
 
     def norm(self, n):
         return nat.normalize(n, self.assumptions)
+
+    def vec_hint(self, flat):
+        """(w, lane) when the access being resolved is lane `lane` of a
+        w-vector (asVector / asScalar) at a w-aligned flat index: flat =
+        base + lane with every coefficient of base a multiple of w."""
+        if not self._vec:
+            return ()
+        w, lane = self._vec[-1]
+        lane = self.norm(lane)
+        if not (isinstance(w, nat.Const) and w.value in (2, 4) and isinstance(lane, nat.Var)):
+            return ()
+        base = self.norm(flat - lane)
+        if lane.name in nat.free_vars(base):
+            return ()
+        # w | base: every monomial has a coefficient divisible by w or a size
+        # variable the unit assumes divisible by w (e.g. the row length m of
+        # `row |> asVector(2)` under 2 | m)
+        divisible = {num.name for num, den in self.assumptions
+                     if isinstance(num, nat.Var) and isinstance(den, nat.Const) and den.value % w.value == 0}
+        for mono, coeff in nat._to_poly(base, ()).items():
+            if coeff % w.value and not any(isinstance(a, nat.Var) and a.name in divisible for a, _p in mono):
+                return ()
+        return (w.value, lane.name)
+
+    def _with_vec(self, w, lane, fn):
+        self._vec.append((w, lane))
+        try:
+            return fn()
+        finally:
+            self._vec.pop()
 
     def clamp(self, inner, hi):
         inner = self.norm(inner)
@@ -366,7 +399,8 @@ class Builder:
                     raise EmitError("tuple projection reached array memory; zips must stay views")
                 buf = self.buffers[b.buf]
                 idx = tuple(self.norm(i) for i in pending) if not buf.deref else ()
-                return Load(buf.name, self.flat(buf, list(pending)), buf.ctype, idx)
+                flat = self.flat(buf, list(pending))
+                return Load(buf.name, flat, buf.ctype, idx, self.vec_hint(flat) if not buf.deref else ())
             raise EmitError(f"cannot read {p!r}")
         if isinstance(p, dpia.PhraseLiteral):
             return Lit(p.text, _lit_ctype(p))
@@ -381,6 +415,14 @@ class Builder:
                 chunk = ta[0]
                 c, j, *rest = pending
                 return self.exp(a0, env, (c * chunk + j, *rest), projs)
+            if tag == "asVector":  # split(w), and the access is lane j of a w-vector
+                chunk = ta[0]
+                c, j, *rest = pending
+                return self._with_vec(chunk, j, lambda: self.exp(a0, env, (c * chunk + j, *rest), projs))
+            if tag == "asScalar":  # join: the flat index's vector lane is f % w
+                inner = ta[1]
+                f, *rest = pending
+                return self.exp(a0, env, (nat.Div(f, inner), nat.Mod(f, inner), *rest), projs)
             if tag == "join":
                 inner = ta[1]
                 f, *rest = pending
@@ -449,7 +491,8 @@ class Builder:
                         raise EmitError(f"indexing into scalar {b.scalar.name}")
                     return b.scalar
                 buf = self.buffers[b.buf]
-                return Store(buf.name, self.flat(buf, idx), buf.ctype)
+                flat = self.flat(buf, idx)
+                return Store(buf.name, flat, buf.ctype, self.vec_hint(flat))
             raise EmitError(f"cannot write through {p!r}")
         if isinstance(p, dpia.ImpPrim):
             tag = p.tag
@@ -461,6 +504,14 @@ class Builder:
                 inner = ta[1]
                 a, b, *rest = pending
                 return self.acc(p.args[0], env, (a * inner + b, *rest))
+            if tag == "asScalarAcc":  # joinAcc, and the write is lane b of a w-vector
+                inner = ta[1]
+                a, b, *rest = pending
+                return self._with_vec(inner, b, lambda: self.acc(p.args[0], env, (a * inner + b, *rest)))
+            if tag == "asVectorAcc":  # splitAcc
+                chunk = ta[0]
+                f, *rest = pending
+                return self.acc(p.args[0], env, (nat.Div(f, chunk), nat.Mod(f, chunk), *rest))
             if tag == "splitAcc":
                 chunk = ta[0]
                 f, *rest = pending

@@ -145,11 +145,17 @@ class Executable:
         if self._temps is None:
             import torch
 
-            self._temps = {
-                t["name"]: torch.empty(max(1, self.temp_sizes[t["name"]]),
-                                       dtype=_torch_dtype(t["ctype"]), device="cuda")
-                for t in self.plan["temps"]
-            }
+            # temporaries with disjoint stage lifetimes share a slot (plan "slot",
+            # emit_cuda.reuse_slots): one allocation of the largest, viewed per type
+            sizes = {}
+            for t in self.plan["temps"]:
+                k = t.get("slot", t["name"])
+                sizes[k] = max(sizes.get(k, 1), self.temp_sizes[t["name"]])
+            slots = {k: torch.empty(n, dtype=torch.float32, device="cuda") for k, n in sizes.items()}
+            self._temps = {}
+            for t in self.plan["temps"]:
+                buf = slots[t.get("slot", t["name"])][: max(1, self.temp_sizes[t["name"]])]
+                self._temps[t["name"]] = buf if t["ctype"] == "float" else buf.view(_torch_dtype(t["ctype"]))
             for st, *_ in self.kernels:
                 for ws in st.get("workspace", []):
                     size = eval_py(ws["size"], self.nats)

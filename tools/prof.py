@@ -11,7 +11,6 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
-sys.path.insert(0, str(ROOT / "bench_support"))
 
 
 def main():
@@ -26,9 +25,9 @@ def main():
     from paper_2201_03611_b200.run import Executable
 
     wl = bench.WORKLOADS[args.workload]()
-    compiled, nats = wl.compile()
+    compiled, nats, host = wl.local()
     exe = Executable(emit_cuda(compiled.unit, **wl.emit_kwargs), nats)
-    dev = [torch.from_numpy(h.reshape(-1)).to("cuda") for h in wl.inputs()]
+    dev = [torch.from_numpy(h.reshape(-1)).to("cuda") for h in host]
     out = torch.empty(exe.output_size, dtype=torch.float32, device="cuda")
     for _ in range(args.iters):
         exe(*dev, out=out)

@@ -384,6 +384,11 @@ class SgemmTiled(SgemmNN):
     program = ("the tiled C4 program (programs.SGEMM_TILED: split / transpose / toMem(Local) under mapWorkGroup / "
                "mapLocal, K tiles) -> the tcgen05 3xTF32 template")
 
+    def compile(self):
+        from paper_2201_03611_b200 import programs
+
+        return programs.compile_config(self.key), self.sizes()
+
 
 class Nbody(Workload):
     key = "nbody"

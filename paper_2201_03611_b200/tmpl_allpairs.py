@@ -44,6 +44,7 @@ RB = int(os.environ.get("RISE_ALLPAIRS_RB", "4"))  # targets per thread
 JT = int(os.environ.get("RISE_ALLPAIRS_JT", "32"))  # sources per warp tile (measured: 32 > 64 > 16)
 UNROLL = int(os.environ.get("RISE_ALLPAIRS_UNROLL", "4"))  # source loop unroll
 PACKED = os.environ.get("RISE_ALLPAIRS_PACKED", "1") == "1"  # two targets per FFMA2/FADD2/FMUL2
+MINB = int(os.environ.get("RISE_ALLPAIRS_MINB", "0"))  # __launch_bounds__ min blocks per SM (0: none)
 
 
 def _split(body):
@@ -225,7 +226,8 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     nthreads = 32 * split
     peer = int(getattr(prog, "peer_ranks", 0) or 0)
     extra = ["const unsigned long long* __restrict__ rs_peer"] if peer else []
-    lines = kernel_head(prog, name, temps, launch_bounds=nthreads, extra_params=extra)
+    lines = kernel_head(prog, name, temps, launch_bounds=f"{nthreads}, {MINB}" if MINB else nthreads,
+                        extra_params=extra)
     lines += [
         f"  constexpr int RS_NT = {r(NT)}, RS_NS = {r(NS)}, RS_JT = {JT}, RS_RB = {RB}, RS_C = {Cv};",
         f"  constexpr int RS_SPLIT = {split}, RS_CH = (RS_NS + RS_SPLIT - 1) / RS_SPLIT;",

@@ -94,3 +94,14 @@ def test_reference_arm_per_config_line():
 def bench_work(key):
     bench = _bench()
     return bench.WORKLOADS[key](0, 1).work()
+
+
+def test_each_workload_compiles_its_own_program():
+    """Every bench workload emits the unit of the program it names (the C4
+    entry is the tiled program, not the flat one)."""
+    bench = _bench()
+    want = {"gemv": "mv", "gemv_opt": "mv", "dot": "dot", "dot_chunked": "dotChunked", "conv": "conv",
+            "sgemm": "sgemm", "sgemm_nn": "sgemm", "sgemm_tiled": "sgemmTiled", "nbody": "nbody"}
+    for key, unit in want.items():
+        compiled, _nats = bench.WORKLOADS[key](0, 1).compile()
+        assert compiled.unit.name == unit, key

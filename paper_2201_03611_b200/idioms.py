@@ -23,7 +23,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
-from . import lir, tmpl_allpairs, tmpl_gemm, tmpl_iterate, tmpl_rowfold, tmpl_seqfold, tmpl_stencil, tmpl_stencil1d, tmpl_transpose
+from . import lir, tmpl_allpairs, tmpl_gemm, tmpl_gridseq, tmpl_iterate, tmpl_rowfold, tmpl_seqfold, tmpl_stencil, tmpl_stencil1d, tmpl_transpose
 from ._ref import nat
 from .emit_cuda import NatRenderer, ValueRenderer, collapse_global_chain, kernel_head, py_expr
 
@@ -37,11 +37,19 @@ class IdiomKernel:
 
 
 ORDER_PRESERVING = ("_match_rowfold", "_match_stencil", "_match_seqfold", "_match_iterate", "_match_transpose",
-                    "_match_stencil1d")
+                    "_match_stencil1d", "_match_gridseq")
 
 
 def _match_iterate(prog, stage, base_name, temps, exact):
     out = tmpl_iterate.match(prog, stage, base_name, temps, exact)
+    if out is None:
+        return None
+    text, plan = out
+    return IdiomKernel(plan["name"], text, plan)
+
+
+def _match_gridseq(prog, stage, base_name, temps, exact):
+    out = tmpl_gridseq.match(prog, stage, base_name, temps, exact)
     if out is None:
         return None
     text, plan = out
@@ -58,7 +66,7 @@ def _match_seqfold(prog, stage, base_name, temps, exact):
 
 def match(prog, stage, base_name, temps, exact, reassociate=True):
     for matcher in (_match_gemm, _match_gemm_tiled, _match_rowfold, _match_reduce, _match_stencil, _match_allpairs,
-                    _match_seqfold, _match_iterate, _match_transpose, _match_stencil1d):
+                    _match_seqfold, _match_iterate, _match_transpose, _match_stencil1d, _match_gridseq):
         if not reassociate and matcher.__name__ not in ORDER_PRESERVING:
             continue
         out = matcher(prog, stage, base_name, temps, exact)
@@ -601,6 +609,7 @@ LAUNCHERS = {
     "gemm_tc": tmpl_gemm.launch,
     "seqfold": tmpl_seqfold.launch,
     "iterate": tmpl_iterate.launch,
+    "gridseq": tmpl_gridseq.launch,
     "transpose2d": tmpl_transpose.launch,
     "stencil1d": tmpl_stencil1d.launch,
 }

@@ -272,3 +272,20 @@ def test_strategy_rules_are_registered_for_strategy_files():
 
     for name in ("splitReduce", "splitMap", "insertToMemReduce", "stageToMem"):
         assert name in rules.RULES and name in rules.RULE_PARAMS
+
+
+def test_tiled_sgemm_other_tile_sizes_are_recognised():
+    """The tiled matcher is not tied to the program's constants: 4-row
+    blocks and K tiles of 16 (and the Bt form through the same staging)
+    are the same contraction."""
+    from paper_2201_03611_b200._ref import nat
+
+    src = programs.SGEMM_TILED.replace("split(2)", "split(4)").replace("split(32)", "split(16)")
+    asm = [(nat.Var("n"), nat.Const(4)), (nat.Var("k"), nat.Const(16))]
+    st = emit_cuda(compile_program(src, None, name="sgemmTiled", assumptions=asm).unit).plan["stages"][0]
+    assert st["kind"] == "gemm_tc" and st["b_major"] == "mn"
+    bt = (programs.SGEMM_TILED.replace("B: Array[k, Array[m, f32]]", "Bt: Array[m, Array[k, f32]]")
+          .replace("transpose(B)", "Bt"))
+    st = emit_cuda(compile_program(bt, None, name="sgemmTiled",
+                                   assumptions=programs.sgemm_tiled_assumptions()).unit).plan["stages"][0]
+    assert st["kind"] == "gemm_tc" and st["b_major"] == "k"

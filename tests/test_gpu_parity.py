@@ -489,3 +489,27 @@ def test_sgemm_tiled_program_on_the_tensor_cores(gpu, n, m, k):
     if oracle.ref_lib() is not None:
         ref = oracle.ref_sgemm_bt(A, Bt)
         assert np.all(np.abs(got - ref) <= 2 * bound)
+
+
+def test_sgemm_tiled_variants_on_the_tensor_cores(gpu):
+    """4-row work-group blocks, K tiles of 16, and the Bt form of the tiled
+    program: claimed by gemm_tc, within the fp64 bound everywhere."""
+    from paper_2201_03611_b200 import compile_program
+    from paper_2201_03611_b200._ref import nat
+
+    n, m, k = 512, 384, 1024
+    A = oracle.rng_inputs(4, n, k)
+    B = oracle.rng_inputs(24, k, m)
+    Bt = np.ascontiguousarray(B.T)
+    C64, absC = _gemm_f64(A, Bt)
+    src = programs.SGEMM_TILED.replace("split(2)", "split(4)").replace("split(32)", "split(16)")
+    c = compile_program(src, None, name="sgemmTiled",
+                        assumptions=[(nat.Var("n"), nat.Const(4)), (nat.Var("k"), nat.Const(16))])
+    bt_src = (programs.SGEMM_TILED.replace("B: Array[k, Array[m, f32]]", "Bt: Array[m, Array[k, f32]]")
+              .replace("transpose(B)", "Bt"))
+    c2 = compile_program(bt_src, None, name="sgemmTiled", assumptions=programs.sgemm_tiled_assumptions())
+    for unit, operand in ((c.unit, B), (c2.unit, Bt)):
+        code = emit_cuda(unit)
+        assert code.plan["stages"][0]["kind"] == "gemm_tc"
+        got = run_cuda(code, unit, {"n": n, "m": m, "k": k}, [A, operand], as_numpy=True).reshape(n, m)
+        assert np.all(np.abs(got - C64) <= oracle.gemm_bound(k, absC))

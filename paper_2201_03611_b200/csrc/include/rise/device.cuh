@@ -195,5 +195,27 @@ RS_DEVICE unsigned rs_xchg_get(const unsigned long long* slot, unsigned epoch) {
   }
 }
 
+// Epoch-tagged 64-bit slot inside one GPU (epoch << 32 | payload bits): one
+// relaxed store publishes tag and payload together (single-copy atomic), so
+// neither side needs a fence; the reader spins until the slot carries its
+// epoch.  A launch that never publishes makes the reader trap after ~20 s.
+RS_DEVICE void rs_slot_put(unsigned long long* slot, unsigned epoch, unsigned payload) {
+  const unsigned long long v = ((unsigned long long)epoch << 32) | payload;
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(slot), "l"(v) : "memory");
+}
+RS_DEVICE unsigned rs_slot_get(const unsigned long long* slot, unsigned epoch) {
+  unsigned long long v, t0, t;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(slot) : "memory");
+  if ((unsigned)(v >> 32) == epoch) return (unsigned)v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    __nanosleep(32);
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(slot) : "memory");
+    if ((unsigned)(v >> 32) == epoch) return (unsigned)v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) __trap();
+  }
+}
+
 RS_DEVICE unsigned rs_lane() { return threadIdx.x & 31u; }
 RS_DEVICE unsigned rs_warp() { return threadIdx.x >> 5; }

@@ -341,6 +341,12 @@ def _match_reduce(prog, stage, base_name, temps, exact):
     def add(a, b):
         return f"__fadd_rn({a}, {b})" if (ct == "float" and exact) else f"({a} + {b})"
 
+    def to_bits(v):
+        return f"__float_as_uint({v})" if ct == "float" else f"(unsigned)({v})"
+
+    def from_bits(v):
+        return f"__uint_as_float({v})" if ct == "float" else f"(int)({v})"
+
     def term_with(u, comp):
         def hook(ld):
             if ld in streams:
@@ -369,7 +375,9 @@ def _match_reduce(prog, stage, base_name, temps, exact):
     peers = int(getattr(prog, "peer_ranks", 0) or 0)
     if peers and not (tma and ct == "float"):
         return None
-    xparams = [f"{ct}* __restrict__ rs_partials", "unsigned* __restrict__ rs_ticket"]
+    # block partials as epoch-tagged 64-bit slots and a 64-bit launch counter
+    # (no fence on the critical path: see phase 3 below)
+    xparams = ["unsigned long long* __restrict__ rs_partials", "unsigned long long* __restrict__ rs_ticket"]
     if peers:
         # multi-GPU: the ranks' totals meet in peer memory (table: R slot arrays, then this rank)
         xparams += ["const unsigned long long* __restrict__ rs_xtab", "unsigned* __restrict__ rs_epoch"]
@@ -505,6 +513,7 @@ def _match_reduce(prog, stage, base_name, temps, exact):
         f"  for (int rs_o = 16; rs_o > 0; rs_o >>= 1) rs_s = {add('rs_s', shfl)};",
         f"  __shared__ {ct} rs_w[{W}];",
         "  __shared__ bool rs_last;",
+        "  __shared__ unsigned rs_ep;",
         "  if ((threadIdx.x & 31) == 0 && threadIdx.x < RS_B) rs_w[threadIdx.x >> 5] = rs_s;",
         "  __syncthreads();",
         "  // phase 3: block butterfly over the warp totals (warp 0)",
@@ -513,10 +522,14 @@ def _match_reduce(prog, stage, base_name, temps, exact):
         "#pragma unroll",
         f"    for (int rs_o = 16; rs_o > 0; rs_o >>= 1) rs_s = {add('rs_s', shfl)};",
         "    if (threadIdx.x == 0) {",
-        "      rs_partials[blockIdx.x] = rs_s;",
-        "      unsigned rs_prev;  // release: the partial is visible before the ticket; acquire for the last block",
-        "      asm volatile(\"atom.add.acq_rel.gpu.u32 %0, [%1], 1;\" : \"=r\"(rs_prev) : \"l\"(rs_ticket) : \"memory\");",
-        "      rs_last = rs_prev == gridDim.x - 1;",
+        "      // a relaxed ticket (the launch counter never resets: launch L takes tickets",
+        "      // [L*G, (L+1)*G), so its epoch is L + 1), then the partial published with",
+        "      // its epoch in ONE 64-bit store — no release fence before the ticket, no",
+        "      // acquire after it: the last block spins until every slot carries the epoch",
+        "      const unsigned long long rs_t = atomicAdd(rs_ticket, 1ull);",
+        "      rs_ep = (unsigned)(rs_t / RS_G) + 1u;",
+        f"      rs_slot_put(rs_partials + blockIdx.x, rs_ep, {to_bits('rs_s')});",
+        "      rs_last = rs_t % RS_G == RS_G - 1;",
         "    }",
         "  }",
         "  __syncthreads();",
@@ -524,7 +537,7 @@ def _match_reduce(prog, stage, base_name, temps, exact):
         "  // phase 4 (last block): thread-strided left folds of the block partials, then butterflies",
         f"  {ct} rs_p = {zero};",
         "  for (int rs_b = threadIdx.x; rs_b < RS_G; rs_b += RS_B) {",
-        f"    rs_p = {add('rs_p', '__ldcg(rs_partials + rs_b)')};",
+        f"    rs_p = {add('rs_p', from_bits('rs_slot_get(rs_partials + rs_b, rs_ep)'))};",
         "  }",
         "  rs_s = rs_p;",
         "#pragma unroll",
@@ -568,7 +581,6 @@ def _match_reduce(prog, stage, base_name, temps, exact):
     for s_ in post:
         lines += [("      " + x) for x in thread_lines(prog, s_, exact)]
     lines += [
-        "      *rs_ticket = 0u;",
         "    }",
         "  }",
         "}",
@@ -584,8 +596,8 @@ def _match_reduce(prog, stage, base_name, temps, exact):
         "pre": pre,
         "fmad": False,
         "order": "reassociated",
-        "workspace": [{"name": ws_p, "ctype": ct, "size": str(G)},
-                      {"name": ws_t, "ctype": "int", "size": "1"}],
+        "workspace": [{"name": ws_p, "ctype": "int", "size": str(2 * G)},  # G 64-bit slots
+                      {"name": ws_t, "ctype": "int", "size": "2"}],  # one 64-bit counter
         "extra_args": [{"kind": "workspace", "name": ws_p}, {"kind": "workspace", "name": ws_t}],
     }
     if peers:

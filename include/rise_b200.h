@@ -146,6 +146,9 @@ int rs_event_elapsed_ms(float* ms, void* start, void* end);
 int rs_graph_capture_begin(void* stream);
 int rs_graph_capture_end(void* stream, void** graph_exec);
 int rs_graph_launch(void* graph_exec, void* stream);
+/* Upload the graph's work to the device ahead of its first launch (the
+ * first launch then pays no upload: cuGraphUpload). */
+int rs_graph_upload(void* graph_exec, void* stream);
 int rs_graph_destroy(void* graph_exec);
 
 /* ---- TMA ------------------------------------------------------------- */

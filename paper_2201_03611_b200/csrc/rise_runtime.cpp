@@ -78,6 +78,7 @@ struct Driver {
   CUresult (*StreamEndCapture)(CUstream, CUgraph*);
   CUresult (*GraphInstantiate)(CUgraphExec*, CUgraph, unsigned long long);
   CUresult (*GraphLaunch)(CUgraphExec, CUstream);
+  CUresult (*GraphUpload)(CUgraphExec, CUstream);
   CUresult (*GraphExecDestroy)(CUgraphExec);
   CUresult (*GraphDestroy)(CUgraph);
   CUresult (*IpcGetMemHandle)(CUipcMemHandle*, CUdeviceptr);
@@ -138,6 +139,7 @@ int load_driver() {
   ok &= sym(g_drv.StreamEndCapture, "cuStreamEndCapture");
   ok &= sym(g_drv.GraphInstantiate, "cuGraphInstantiateWithFlags");
   ok &= sym(g_drv.GraphLaunch, "cuGraphLaunch");
+  ok &= sym(g_drv.GraphUpload, "cuGraphUpload");
   ok &= sym(g_drv.GraphExecDestroy, "cuGraphExecDestroy");
   ok &= sym(g_drv.GraphDestroy, "cuGraphDestroy");
   ok &= sym(g_drv.IpcGetMemHandle, "cuIpcGetMemHandle");
@@ -602,6 +604,12 @@ int rs_graph_capture_end(void* stream, void** graph_exec) {
 int rs_graph_launch(void* graph_exec, void* stream) {
   if (int e = ensure_ctx()) return e;
   CU(g_drv.GraphLaunch((CUgraphExec)graph_exec, (CUstream)stream), "cuGraphLaunch");
+  return 0;
+}
+
+int rs_graph_upload(void* graph_exec, void* stream) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.GraphUpload((CUgraphExec)graph_exec, (CUstream)stream), "cuGraphUpload");
   return 0;
 }
 

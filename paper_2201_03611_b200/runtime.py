@@ -35,7 +35,7 @@ EXPORTED = (
     "rs_event_destroy", "rs_event_record", "rs_event_synchronize", "rs_event_elapsed_ms",
     "rs_tma_desc_2d_f32", "rs_ipc_handle", "rs_ipc_open", "rs_ipc_close", "rs_halo_exchange",
     "rs_comm_unique_id", "rs_comm_init", "rs_comm_destroy", "rs_allgather",
-    "rs_graph_capture_begin", "rs_graph_capture_end", "rs_graph_launch", "rs_graph_destroy",
+    "rs_graph_capture_begin", "rs_graph_capture_end", "rs_graph_launch", "rs_graph_upload", "rs_graph_destroy",
 )
 
 _lib = None
@@ -105,6 +105,7 @@ def lib():
             L.rs_graph_capture_begin.argtypes = [vp]
             L.rs_graph_capture_end.argtypes = [vp, ctypes.POINTER(vp)]
             L.rs_graph_launch.argtypes = [vp, vp]
+            L.rs_graph_upload.argtypes = [vp, vp]
             L.rs_graph_destroy.argtypes = [vp]
             _lib = L
     return _lib
@@ -511,6 +512,11 @@ class Graph:
 
     def __call__(self):
         check_run(lib().rs_graph_launch(self.h, self.stream), "rs_graph_launch")
+
+    def upload(self):
+        """Move the graph's work to the device now (cuGraphUpload), so the
+        first replay starts without the upload."""
+        check_run(lib().rs_graph_upload(self.h, self.stream), "rs_graph_upload")
 
     def __del__(self):
         try:

@@ -487,6 +487,8 @@ def config_of(wl, n_gpus):
         "sizes": wl.sizes(),
         "n_gpus": n_gpus,
         "parallelism": "1 GPU" if n_gpus == 1 else wl.parallelism(),
+        "l2": ("inputs larger than L2 (>= 512 MiB of input sets used round robin)" if wl.bound == "hbm"
+               else "L2 flushed between steps (256 MiB write + read, outside the events)"),
         "per_config": list(PER_CONFIG),
     }
 

@@ -41,10 +41,18 @@ import os
 # on B200: SPLIT 1 / 4 / 8 / 16 -> 0.52 / 0.63 / 0.67 / 0.67 of FP32 peak
 SPLIT = int(os.environ.get("RISE_ALLPAIRS_SPLIT", "16"))
 RB = int(os.environ.get("RISE_ALLPAIRS_RB", "4"))  # targets per thread
-JT = int(os.environ.get("RISE_ALLPAIRS_JT", "32"))  # sources per warp tile (measured: 32 > 64 > 16)
-UNROLL = int(os.environ.get("RISE_ALLPAIRS_UNROLL", "4"))  # source loop unroll
+# sources per warp tile, source-loop unroll and __launch_bounds__ min blocks
+# per SM (0: none).  Measured at 131072 bodies (round 2, one B200):
+#   JT 32, unroll 4, no min            0.684 of the FP32 peak (round-1 default)
+#   min 1 (the compiler may use up to 128 registers: one 16-warp block per SM,
+#   and a schedule that overlaps more of the r2 -> rsqrt -> scale chains)
+#         unroll 4 / 8 / 16            0.686 / 0.691 / 0.691
+#   min 1, JT 64, unroll 8 / 16 / 64   0.702 / 0.702 / 0.702   <- default
+#   JT 64 without min 1                0.680; min 2 / 3-6        0.678 / 0.60-0.65
+JT = int(os.environ.get("RISE_ALLPAIRS_JT", "64"))
+UNROLL = int(os.environ.get("RISE_ALLPAIRS_UNROLL", "8"))
 PACKED = os.environ.get("RISE_ALLPAIRS_PACKED", "1") == "1"  # two targets per FFMA2/FADD2/FMUL2
-MINB = int(os.environ.get("RISE_ALLPAIRS_MINB", "0"))  # __launch_bounds__ min blocks per SM (0: none)
+MINB = int(os.environ.get("RISE_ALLPAIRS_MINB", "1"))
 
 
 def _split(body):

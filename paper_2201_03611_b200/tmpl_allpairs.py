@@ -247,10 +247,9 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     lines += [
         # one source tile per warp: the warps of a block fold disjoint source
         # chunks for the same targets, so a warp only ever syncs with itself
-        # (dynamic shared memory: the source tiles, later reused for the chunk partials)
-        "  extern __shared__ __align__(16) float rs_dyn[];",
+        f"  __shared__ __align__(16) float rs_sm[RS_SPLIT][RS_JT * {rec}];",
         "  const int rs_w = threadIdx.x >> 5, rs_l = threadIdx.x & 31;",
-        f"  float* const rs_s = rs_dyn + rs_w * (RS_JT * {rec});",
+        "  float* const rs_s = rs_sm[rs_w];",
         "  const int rs_g0 = blockIdx.x * (32 * RS_RB) + rs_l;",
         "  int rs_j0 = 0;",
         f"  auto rs_step = [&](const int {gv}, {cdecl}, const int {j}, {acc.ctype} {acc.name}) -> {acc.ctype} {{",
@@ -333,10 +332,8 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     if split > 1:
         add = "__fadd_rn" if acc.ctype == "float" else ""
         lines += [
-            # chunk partials meet in shared memory (the tiles' space, once every warp
-            # is done with its tile) and are added in chunk order
-            "  __syncthreads();",
-            f"  {acc.ctype} (*const rs_part)[RS_RB * RS_C][32] = reinterpret_cast<{acc.ctype} (*)[RS_RB * RS_C][32]>(rs_dyn);",
+            # chunk partials meet in shared memory and are added in chunk order
+            f"  __shared__ {acc.ctype} rs_part[RS_SPLIT - 1][RS_RB * RS_C][32];",
             "  if (rs_w > 0) {",
             "#pragma unroll",
             "    for (int rs_r = 0; rs_r < RS_RB; ++rs_r)",
@@ -366,11 +363,9 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
     ]
     lines += post_lines
     lines += ["      }", "    }", "  }", "}"]
-    smem = max(split * JT * rec * 4, (split - 1) * RB * Cv * 32 * 4 if split > 1 else 0)
     plan = {
         "name": name,
         "kind": "allpairs",
-        "smem": smem,
         "targets": py_expr(NT),
         "per_block": 32 * RB,
         "block": nthreads,
@@ -390,4 +385,4 @@ def launch(st, nats, sm):
     from .emit_cuda import eval_py
 
     nt = eval_py(st["targets"], nats)
-    return (max(1, -(-nt // st["per_block"])), 1, 1), (st["block"], 1, 1), st.get("smem", 0), (1, 1, 1)
+    return (max(1, -(-nt // st["per_block"])), 1, 1), (st["block"], 1, 1), 0, (1, 1, 1)

@@ -332,9 +332,12 @@ class GenericKernel:
             for ld in lir.expr_loads(x.value):
                 if ld.vec == (w, v) and ld.ctype == "float" and ld.buf not in written:
                     loads.setdefault((ld.buf, base_of(ld.index)), f"rs_vl{len(loads)}")
+        scalar_written = {x.target.buf for x in body
+                          if isinstance(x.target, lir.Store) and not (x.target.vec == (w, v) and x.target.ctype == "float")}
         for x in body:
             t = x.target
-            if isinstance(t, lir.Store) and t.vec == (w, v) and t.ctype == "float" and t.buf not in read:
+            if (isinstance(t, lir.Store) and t.vec == (w, v) and t.ctype == "float" and t.buf not in read
+                    and t.buf not in scalar_written):
                 key = (t.buf, base_of(t.index))
                 if key in stores:
                     return None  # a lane written twice: keep the scalar order

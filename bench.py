@@ -905,6 +905,8 @@ def _time_with_gather(ctx, wl, exe, dev_in, out, stream, steps, warmup):
 
     dist, rank, world = ctx.dist, ctx.rank, ctx.world
     native = dist.get_backend() == "nccl"
+    if wl.key.startswith("gemv") and wl.scaling == "strong" and os.environ.get("RISE_GEMV_PEER_Y", "1") == "1":
+        return _time_fused_y(ctx, wl, exe, dev_in, stream, steps, warmup)
     if wl.key.startswith("sgemm"):
         recv = dev_in[1]
         send = recv.view(world, -1)[rank].clone()
@@ -952,6 +954,49 @@ def _time_with_gather(ctx, wl, exe, dev_in, out, stream, steps, warmup):
     return {"value": round(wl.total_work() / (ms * 1e-3) / 1e9, 3), "unit": wl.metric_unit,
             "ms_per_step": round(ms, 6), "collective": what,
             "bytes_gathered_per_rank": int(recv.numel() * recv.element_size())}
+
+
+def _time_fused_y(ctx, wl, exe, dev_in, stream, steps, warmup):
+    """gemv with y all-gathered INSIDE the kernel: the rowfold kernel emitted
+    with peer_out=N stores every row into every rank's full y (peer memory
+    over NVLink) and the ranks meet once per launch in epoch-tagged slots
+    (shard.PeerOutput) — one kernel per step, no collective call."""
+    import torch
+
+    from paper_2201_03611_b200 import emit_cuda, shard
+    from paper_2201_03611_b200.run import Executable
+
+    dist, world = ctx.dist, ctx.world
+    compiled, nats, _host = wl.local()
+    fused = Executable(emit_cuda(compiled.unit, peer_out=world), nats, device=ctx.device)
+    full = torch.zeros(wl.n, dtype=torch.float32, device="cuda")
+    r0, _r1 = wl.band(wl.n)
+    torch.cuda.synchronize()
+    po = shard.PeerOutput(full, r0)
+    out = torch.empty(fused.output_size, dtype=torch.float32, device="cuda")
+    launch = _bound_launch(fused, dev_in, out, stream, po.extra)
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            launch()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(steps):
+            launch()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = ctx.max_over_ranks(e0.elapsed_time(e1) / steps)
+    po.close()
+    return {"value": round(wl.total_work() / (ms * 1e-3) / 1e9, 3), "unit": wl.metric_unit,
+            "ms_per_step": round(ms, 6),
+            "collective": ("y all-gathered inside the rowfold kernel: every row stored into every rank's full y over "
+                           "NVLink (peer stores), epoch-tagged completion slots (emit_cuda peer_out); one kernel per "
+                           "step, no collective call"),
+            "bytes_gathered_per_rank": int(full.numel() * 4)}
 
 
 _COMM = []
@@ -1166,6 +1211,10 @@ def _alt_reference(wl, host):
 def run_reference(args, rank, world):
     if rank != 0:
         return None
+    # every host core (torchrun sets OMP_NUM_THREADS=1 per rank; the
+    # reference's OpenMP C is the only work on this host here): set before the
+    # OpenMP runtime of oracle/_ref is loaded
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     import oracle
 
     if oracle.ref_lib() is None:

@@ -624,7 +624,8 @@ class SingleBlockStage(UserWarning):
     """A kernel stage that runs in one block / one thread on the GPU."""
 
 
-def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, peer_halo=False) -> CudaCode:
+def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, peer_halo=False,
+              peer_out=0) -> CudaCode:
     """Emit the sm100a kernel text (and launch plan) for an ImperativeUnit.
 
     `reassociate=False` keeps every reduction in the program's own order
@@ -637,6 +638,13 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, pee
     in place through a device table of peer pointers (extra launch argument
     `rs_peer_table`), fusing the all-gather of the sources into the fold.
 
+    `peer_out=R` (multi-GPU row bands whose result is all-gathered): the
+    `rowfold` template also stores every row's value into every rank's
+    full-result buffer (extra launch arguments `rs_y_table`: R peer pointers
+    and this rank's row offset; `rs_peer_table`: the completion slots), and
+    the ranks meet once per launch in epoch-tagged slots — the all-gather
+    fused into the GEMV.
+
     `peer_halo=True` (multi-GPU row bands): the `stencil2d` template reads
     the rows padClamp would invent above / below the band from the
     neighbours' bands in place (extra launch arguments `rs_halo_top` /
@@ -647,6 +655,7 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, pee
     prog = lir.build(unit)
     prog.peer_ranks = int(peer_ranks)
     prog.peer_halo = bool(peer_halo)
+    prog.peer_out = int(peer_out)
     stages, temps = split_stages(prog.body, prog)
     kernels = []
     plan_stages = []
@@ -662,6 +671,8 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, pee
                             "reduce template (totals exchanged in peer memory) takes")
         if peer_halo and (match is None or not match.plan.get("peer_halo")):
             raise EmitError("peer_halo needs a stage the stencil2d template takes (halo rows read in place)")
+        if peer_out and (match is None or not match.plan.get("peer_out")):
+            raise EmitError("peer_out needs a stage the rowfold template takes (rows stored into every rank)")
         if match is not None:
             kernels.append(match.text)
             for inc in match.includes:
@@ -721,6 +732,8 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, pee
         plan["peer_halo"] = True
     if peer_ranks:
         plan["peer_ranks"] = int(peer_ranks)
+    if peer_out:
+        plan["peer_out"] = int(peer_out)
         peers = {b for st in plan_stages for b in st.get("peer_streams", [])}
         for spec in plan["inputs"]:
             if spec["name"] in peers:

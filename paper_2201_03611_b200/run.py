@@ -69,7 +69,7 @@ class Executable:
         for st in self.plan["stages"]:
             chosen = st
             if st.get("pre") and not all(eval_py(p, self.nats) for p in st["pre"]):
-                if st.get("peer_ranks") or st.get("peer_halo"):
+                if st.get("peer_ranks") or st.get("peer_halo") or st.get("peer_out"):
                     raise InterpreterError(f"{st['name']}: sizes {self.nats} fail the peer-memory variant's "
                                            f"preconditions {st['pre']} (no fallback reads peers)")
                 chosen = st["fallback"]
@@ -80,8 +80,8 @@ class Executable:
             # bulk copies, TMA): its generic kernel is compiled beside it and runs
             # instead when a caller's buffer is not 16-byte aligned (e.g. x[1:])
             # (compiled on first use: some generic kernels only compile at small sizes)
-            fb = chosen.get("fallback") if chosen is st and not (st.get("peer_ranks") or st.get("peer_halo")) \
-                else None
+            fb = chosen.get("fallback") if chosen is st and not (
+                st.get("peer_ranks") or st.get("peer_halo") or st.get("peer_out")) else None
             self.launches.append((chosen, name_expr, fb))
         self._opts = ["--fmad=true" if fmad else "--fmad=false"]
         self.module = rt.load_module(text, exprs, self._opts, program_name=f"{self.plan['unit']}.cu")
@@ -247,6 +247,11 @@ class Executable:
         if kind == "peer_ptr":  # optional: absent / None / 0 -> NULL (e.g. the image's real edge)
             value = buffers.get(extra["name"])
             return ctypes.c_void_p(0 if value is None else _dptr(value) if hasattr(value, "data_ptr") else int(value))
+        if kind == "peer_ptr_table":  # e.g. rs_y_table: R peer pointers + this rank's offset (int64 tensor)
+            table = buffers.get(extra["name"])
+            if table is None:
+                raise InterpreterError(f"peer-output kernel launched without buffers[{extra['name']!r}]")
+            return ctypes.c_void_p(_dptr(table))
         if kind == "peer_table":
             table = buffers.get("rs_peer_table")
             if table is None:

@@ -302,3 +302,47 @@ class PeerHaloRows:
         for p in self.opened:
             runtime.ipc_close(p)
         self.opened = []
+
+
+class PeerOutput:
+    """The full-result buffers of a `rowfold` kernel emitted with
+    peer_out=R (gemv row bands whose y is all-gathered inside the kernel):
+    every rank owns a full-length result buffer (`full`, device tensor),
+    exports it (CUDA IPC), maps everyone else's, and hands the kernel
+    `extra["rs_y_table"]` = [R buffer pointers (rank order), this rank's
+    first row] — each row's value lands in every rank's buffer at that
+    offset — and `extra["rs_peer_table"]`, the completion slots
+    (`PeerExchange`): the kernel's last block publishes the launch's epoch to
+    every rank and waits for every rank's, so when the kernel has finished,
+    this rank's `full` holds every rank's rows."""
+
+    def __init__(self, full, row_offset: int, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import runtime
+
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, runtime.ipc_handle(full.data_ptr()), group=group)
+        self.opened = []
+        ptrs = []
+        for r in range(self.world):
+            if r == self.rank:
+                ptrs.append(int(full.data_ptr()))
+            else:
+                p = runtime.ipc_open(*everyone[r])
+                self.opened.append(p)
+                ptrs.append(p)
+        self.full = full
+        self.table = torch.tensor(ptrs + [int(row_offset)], dtype=torch.int64, device="cuda")
+        self.exchange = PeerExchange(group)
+        self.extra = {"rs_y_table": self.table, "rs_peer_table": self.exchange.table}
+
+    def close(self):
+        from . import runtime
+
+        for p in self.opened:
+            runtime.ipc_close(p)
+        self.opened = []
+        self.exchange.close()

@@ -131,6 +131,16 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
     stages_py = (f"({STAGES} if {budget} // ({stage_py} * 4) >= {STAGES} else "
                  f"(1 if {budget} // ({stage_py} * 4) < 1 else {budget} // ({stage_py} * 4)))")
     extra = [f"const __grid_constant__ rs_tmap rs_map{k}" for k in range(len(rs_list))]
+    peer_out = int(getattr(prog, "peer_out", 0) or 0)
+    if peer_out:
+        # multi-GPU row bands with the result all-gathered INSIDE the kernel:
+        # every row's value is also stored into every rank's full-result buffer
+        # (peer memory over NVLink), then the ranks meet once per launch in
+        # epoch-tagged slots (the dot exchange's protocol)
+        if any(t.buf != prog.output.name for s_ in post for t, _v in lir.stmt_exprs(s_) if isinstance(t, lir.Store)):
+            return None
+        extra += ["const unsigned long long* __restrict__ rs_ytab", "const unsigned long long* __restrict__ rs_xtab",
+                  "unsigned long long* __restrict__ rs_ticket"]
     lines = kernel_head(prog, name, temps, launch_bounds=32, extra_params=extra)
     lines += [
         f"  constexpr int RS_NROWS = {r(nrows)};",
@@ -262,7 +272,40 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
     for s in post:
         g = GenericKernel(prog, Stage("serial", s), "_", [], exact)
         lines += [("    " + x) for x in g.thread(s, 0)]
-    lines += ["  }", "}"]
+    if peer_out:
+        out_name = prog.output.name
+        lines += [
+            f"    // the same stores into every rank's full buffer, at this rank's row offset",
+            f"    for (int rs_k = 0; rs_k < {peer_out}; ++rs_k) {{",
+            f"      float* const {out_name} = reinterpret_cast<float*>(rs_ytab[rs_k]) + rs_ytab[{peer_out}];",
+        ]
+        for s_ in post:
+            g = GenericKernel(prog, Stage("serial", s_), "_", [], exact)
+            lines += [("      " + x) for x in g.thread(s_, 0)]
+        lines += ["    }"]
+    lines += ["  }"]
+    if peer_out:
+        lines += [
+            "  // this block's peer stores are visible system-wide before its ticket; the",
+            "  // launch's last block then publishes the epoch to every rank and waits for",
+            "  // every rank's: when the kernel ends, every rank's full buffer is complete",
+            "  __threadfence_system();",
+            "  __syncwarp(RS_MASK);",
+            "  if (rs_lane == 0) {",
+            "    const unsigned long long rs_t = atomicAdd(rs_ticket, 1ull);",
+            "    if (rs_t % gridDim.x == gridDim.x - 1) {",
+            "      const unsigned rs_e = (unsigned)(rs_t / gridDim.x) + 1u;",
+            f"      constexpr int RS_R = {peer_out};",
+            "      const int rs_me = (int)rs_xtab[RS_R];",
+            "      const int rs_bank = (int)(rs_e & 1u) * RS_R;  // two banks by epoch parity (PeerExchange)",
+            "      for (int rs_k = 0; rs_k < RS_R; ++rs_k)",
+            "        rs_xchg_put(reinterpret_cast<unsigned long long*>(rs_xtab[rs_k]) + rs_bank + rs_me, rs_e, 1u);",
+            "      const unsigned long long* rs_slots = reinterpret_cast<const unsigned long long*>(rs_xtab[rs_me]) + rs_bank;",
+            "      for (int rs_k = 0; rs_k < RS_R; ++rs_k) (void)rs_xchg_get(rs_slots + rs_k, rs_e);",
+            "    }",
+            "  }",
+        ]
+    lines += ["}"]
     smem = f"{stages_py} * {stage_py} * 4 + {stages_py} * 8 + 1024"
     plan = {
         "name": name,
@@ -275,4 +318,9 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
         "order": "preserved",
         "extra_args": tmaps,
     }
+    if peer_out:
+        ws_t = f"rs_ws_{name}_ticket"
+        plan.update(peer_out=peer_out, workspace=[{"name": ws_t, "ctype": "int", "size": "2"}])
+        plan["extra_args"] = tmaps + [{"kind": "peer_ptr_table", "name": "rs_y_table"},
+                                      {"kind": "peer_table"}, {"kind": "workspace", "name": ws_t}]
     return "\n".join(lines) + "\n", plan

@@ -363,3 +363,59 @@ def test_gemv_sgemm_row_bands_with_gathers(world):
         assert gemv_kinds == ["rowfold"]
         assert ok_sgemm, f"rank {rank}: gathered sgemm outside the 3xTF32 bound"
         assert sgemm_kinds == ["gemm_tc"]
+
+
+def _peer_y_worker(rank, world, port, q):
+    """gemv row bands whose y is all-gathered INSIDE the rowfold kernel
+    (emit_cuda(peer_out=R), shard.PeerOutput): after each launch every
+    rank's full y equals the whole gemv, launch after launch (epochs)."""
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2201_03611_b200 import emit_cuda, programs, shard
+        from paper_2201_03611_b200.run import Executable
+
+        torch.cuda.set_device(0)
+        n, m = 300, 1024
+        M = oracle.rng_inputs(2, n, m)
+        r0, rows = shard.row_band(n, world, rank)
+        exe = Executable(emit_cuda(programs.compile_config("gemv").unit, peer_out=world), {"n": rows, "m": m})
+        band = torch.from_numpy(np.ascontiguousarray(M[r0:r0 + rows]).reshape(-1)).cuda()
+        full = torch.zeros(n, dtype=torch.float32, device="cuda")
+        torch.cuda.synchronize()
+        po = shard.PeerOutput(full, r0)
+        dist.barrier()
+        oks = []
+        for it in range(3):
+            x = oracle.rng_inputs(20 + it, m)
+            y = exe(band, torch.from_numpy(x).cuda(), extra=po.extra)
+            torch.cuda.synchronize()
+            want = oracle.mv(M, x)
+            oks.append(np.array_equal(full.cpu().numpy(), want)
+                       and np.array_equal(y.cpu().numpy(), want[r0:r0 + rows]))
+            dist.barrier()  # every rank has read its full y before the next launch overwrites it
+        kinds = exe.template_kinds
+        dist.barrier()
+        po.close()
+        q.put((rank, oks, kinds))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gemv_y_all_gathered_inside_the_kernel(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_y_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, oks, kinds in res:
+        assert all(oks), f"rank {rank}: the in-kernel all-gather of y differs from the oracle: {oks}"
+        assert kinds == ["rowfold"]

@@ -289,3 +289,19 @@ def test_tiled_sgemm_other_tile_sizes_are_recognised():
     st = emit_cuda(compile_program(bt, None, name="sgemmTiled",
                                    assumptions=programs.sgemm_tiled_assumptions()).unit).plan["stages"][0]
     assert st["kind"] == "gemm_tc" and st["b_major"] == "k"
+
+
+def test_peer_out_emission():
+    """peer_out=R: the rowfold kernel takes the full-result table, the
+    completion slots and a launch counter; programs no rowfold takes refuse
+    (no fallback could write the peers)."""
+    code = emit_cuda(programs.compile_config("gemv").unit, peer_out=4)
+    st = code.plan["stages"][0]
+    assert st["kind"] == "rowfold" and st["peer_out"] == 4 and code.plan["peer_out"] == 4
+    assert [e["kind"] for e in st["extra_args"][-3:]] == ["peer_ptr_table", "peer_table", "workspace"]
+    assert "__threadfence_system();" in code.text and "rs_xchg_get" in code.text
+    names = [f"{st['name']}<2048, 8192>"]
+    cubin, _ = runtime.compile_cubin(code.text, names, ["--fmad=false"])
+    assert cubin[:4] == b"\x7fELF"
+    with pytest.raises(errors.EmitError):
+        emit_cuda(programs.compile_config("conv").unit, peer_out=2)

@@ -730,10 +730,10 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, pee
     }
     if peer_halo:
         plan["peer_halo"] = True
-    if peer_ranks:
-        plan["peer_ranks"] = int(peer_ranks)
     if peer_out:
         plan["peer_out"] = int(peer_out)
+    if peer_ranks:
+        plan["peer_ranks"] = int(peer_ranks)
         peers = {b for st in plan_stages for b in st.get("peer_streams", [])}
         for spec in plan["inputs"]:
             if spec["name"] in peers:

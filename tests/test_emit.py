@@ -305,3 +305,11 @@ def test_peer_out_emission():
     assert cubin[:4] == b"\x7fELF"
     with pytest.raises(errors.EmitError):
         emit_cuda(programs.compile_config("conv").unit, peer_out=2)
+
+
+def test_peer_ranks_marks_the_peer_source_inputs():
+    from paper_2201_03611_b200 import compile_program
+
+    c = compile_program(programs.NBODY_SHARD, None, name="nbodyShard")
+    plan = emit_cuda(c.unit, peer_ranks=2).plan
+    assert {i["name"] for i in plan["inputs"] if i.get("peer")} == {"pos", "mass"}

@@ -49,6 +49,9 @@ RB = int(os.environ.get("RISE_ALLPAIRS_RB", "4"))  # targets per thread
 #         unroll 4 / 8 / 16            0.686 / 0.691 / 0.691
 #   min 1, JT 64, unroll 8 / 16 / 64   0.702 / 0.702 / 0.702   <- default
 #   JT 64 without min 1                0.680; min 2 / 3-6        0.678 / 0.60-0.65
+#   the next tile prefetched into registers during the fold: 0.696 (the
+#   staging latency is not on the critical path); a constant-trip fold loop
+#   for full tiles: no change
 JT = int(os.environ.get("RISE_ALLPAIRS_JT", "64"))
 UNROLL = int(os.environ.get("RISE_ALLPAIRS_UNROLL", "8"))
 PACKED = os.environ.get("RISE_ALLPAIRS_PACKED", "1") == "1"  # two targets per FFMA2/FADD2/FMUL2

@@ -656,6 +656,7 @@ def emit_cuda(unit, exact=True, idioms=True, reassociate=True, peer_ranks=0, pee
     prog.peer_ranks = int(peer_ranks)
     prog.peer_halo = bool(peer_halo)
     prog.peer_out = int(peer_out)
+    prog.reassociate = bool(reassociate)  # (rowfold: split rows for short row counts)
     stages, temps = split_stages(prog.body, prog)
     kernels = []
     plan_stages = []

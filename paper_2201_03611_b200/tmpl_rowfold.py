@@ -39,8 +39,27 @@ ROWS = int(os.environ.get("RISE_ROWFOLD_ROWS", "0"))  # rows per block (8, 16 or
 KT = int(os.environ.get("RISE_ROWFOLD_KT", "256"))  # columns per stage (KT/32 TMA boxes of 32 columns)
 # measured (gemv 8192², L2 flushed, 32-row blocks): 128x6 0.835, 256x2 0.855, 512x2 0.65; (round-robin
 # inputs, 28-row blocks, two passes): 256x2 0.924-0.929, 256x3 0.936-0.939 (chunked dot 0.563 -> 0.583)
-STAGES = int(os.environ.get("RISE_ROWFOLD_STAGES", "3"))
+# ring depth: 0 = as many stages as the block's shared-memory budget holds,
+# up to MAX_STAGES.  A stage's fold is latency-bound (one dependent add per
+# column per lane: 256 columns ~ 0.5 us), so the ring must reach ~ 2-3 us
+# ahead to cover DRAM latency: 3 stages at 8192 rows (32-row boxes, 33 KiB
+# stages), 6 at 4096, 12 at <= 2048 (row bands of strong-scaled gemv)
+STAGES = int(os.environ.get("RISE_ROWFOLD_STAGES", "0"))
+MAX_STAGES = int(os.environ.get("RISE_ROWFOLD_MAX_STAGES", "12"))
+MIN_ROWS = int(os.environ.get("RISE_ROWFOLD_MIN_ROWS", "4"))
+# shared-memory reads issued this many 4-column chunks ahead of their use
+PF = int(os.environ.get("RISE_ROWFOLD_PF", "4"))
 SM_COUNT = 148
+# split rows (reassociating, deterministic): a row's fold is a dependent
+# chain of K adds (~7 cycles each with one warp per SM sub-partition, about
+# 31 us at K = 8192 — tools/probe_chain.cu), so when there are fewer rows
+# than it takes to fill the GPU (strong-scaled row bands) each row is folded
+# as S contiguous column chunks by S adjacent lanes and the chunk partials
+# are added in chunk order: S = the smallest power of two <= 32 with
+# rows * S >= SPLIT_TARGET, for K >= SPLIT_MIN_K.  Only under
+# emit_cuda(reassociate=True) (the default) and only for a sum fold.
+SPLIT_TARGET = int(os.environ.get("RISE_ROWFOLD_SPLIT_TARGET", "8192"))
+SPLIT_MIN_K = int(os.environ.get("RISE_ROWFOLD_SPLIT_MIN_K", "2048"))
 
 
 def rows_per_block(nrows_py):
@@ -49,14 +68,16 @@ def rows_per_block(nrows_py):
 
     One lane folds one row and a block is one warp, so the rows are dealt
     out as evenly as the SMs allow: R = ceil(rows / (2 x 148)) clamped to
-    [8, 32] gives two blocks on (nearly) every SM.  8192 rows -> 28 rows
-    per block, 293 blocks (with 32 rows, 256 blocks leave 40 SMs one block
-    and 108 two: the two-block SMs set the time); 4096 rows -> 14."""
+    [MIN_ROWS, 32] gives two blocks on (nearly) every SM.  8192 rows -> 28
+    rows per block, 293 blocks (with 32 rows, 256 blocks leave 40 SMs one
+    block and 108 two: the two-block SMs set the time); 4096 rows -> 14;
+    1024 (a strong-scaled band at 8 GPUs) -> 4."""
     if ROWS:
         return str(ROWS), str(ROWS)
     slots = 2 * SM_COUNT
-    return (f"(32 if ({nrows_py}) > {32 * slots} else (8 if ({nrows_py}) <= {8 * slots} else -(-({nrows_py}) // {slots})))",
-            f"(RS_NROWS > {32 * slots} ? 32 : RS_NROWS <= {8 * slots} ? 8 : (RS_NROWS + {slots - 1}) / {slots})")
+    lo = MIN_ROWS
+    return (f"(32 if ({nrows_py}) > {32 * slots} else ({lo} if ({nrows_py}) <= {lo * slots} else -(-({nrows_py}) // {slots})))",
+            f"(RS_NROWS > {32 * slots} ? 32 : RS_NROWS <= {lo * slots} ? {lo} : (RS_NROWS + {slots - 1}) / {slots})")
 
 
 def affine_in_flat_row(base, loops, assumptions):
@@ -89,6 +110,14 @@ def affine_in_flat_row(base, loops, assumptions):
     return c0, pitch, pre
 
 
+def _is_sum_step(step, acc):
+    """step == acc + e (or e + acc) with e free of acc, in fp32"""
+    if not (isinstance(step, lir.Bin) and step.op == "+" and step.ctype == "float"):
+        return False
+    other = step.b if step.a == acc else step.a if step.b == acc else None
+    return other is not None and acc not in set(lir.expr_scalars(other))
+
+
 def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_coef):
     """Render the kernel; returns (text, plan) or None if a precondition
     cannot be expressed."""
@@ -99,21 +128,49 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
     for _, b in loops:
         nrows = nrows * b
     nrows = nat.normalize(nrows, prog.assumptions)
-    rows_py, rows_c = rows_per_block(py_expr(nrows))
+    n_py, k_py = py_expr(nrows), py_expr(loop.bound)
 
     rs_list = list(dict.fromkeys(row_streams.values()))
     sh_list = list(dict.fromkeys(shared_streams.values()))
-    # TMA boxes need non-empty tensors; 16-byte bulk copies need K % 4 == 0
-    pre = [f"({py_expr(loop.bound)}) % 4 == 0", f"({py_expr(loop.bound)}) > 0", f"({py_expr(nrows)}) > 0"]
-    tmaps = []
-    for k, (buf, base) in enumerate(rs_list):
+    affs = []
+    for buf, base in rs_list:
         aff = affine_in_flat_row(base, loops, prog.assumptions)
         if aff is None:
             return None
-        c0, pitch, apre = aff
+        affs.append(aff)
+    split = SPLIT_TARGET > 0 and getattr(prog, "reassociate", False) and _is_sum_step(step, acc)
+    if split:
+        # S (a power of two <= 32) from the sizes, the same in Python (plan) and C
+        conds_py = [f"({n_py}) < {SPLIT_TARGET}", f"({k_py}) >= {SPLIT_MIN_K}", f"({k_py}) % 128 == 0"]
+        conds_c = [f"({r(nrows)}) < {SPLIT_TARGET}", f"({r(loop.bound)}) >= {SPLIT_MIN_K}", f"({r(loop.bound)}) % 128 == 0"]
+        for _c0, pitch, _pre in affs:  # the chunks of a row are the rows of a [rows * S][K / S] view
+            conds_py.append(f"({py_expr(pitch)}) == ({k_py})")
+            conds_c.append(f"({r(pitch)}) == ({r(loop.bound)})")
+        s_py = "(1 if not (" + " and ".join(conds_py) + ") else "
+        s_c = "(!(" + " && ".join(conds_c) + ") ? 1 : "
+        for sv in (2, 4, 8, 16):
+            s_py += f"{sv} if ({n_py}) * {sv} >= {SPLIT_TARGET} else "
+            s_c += f"({r(nrows)}) * {sv} >= {SPLIT_TARGET} ? {sv} : "
+        s_py += "32)"
+        s_c += "32)"
+    else:
+        s_py = s_c = "1"
+    nv_py = f"(({n_py}) * {s_py})" if split else n_py
+    kv_py = f"(({k_py}) // {s_py})" if split else k_py
+    rows_py, rows_c = rows_per_block(nv_py)
+    if split:  # a row's S chunks stay in one warp, S-aligned
+        rows_py = f"(-(-({rows_py}) // {s_py}) * {s_py})"
+        rows_c = f"((({rows_c}) + RS_S - 1) / RS_S * RS_S)"
+    xs = KT + 4 if split else KT  # shared-stream segment stride (padded: S segments, conflict-free)
+
+    # TMA boxes need non-empty tensors; 16-byte bulk copies need K % 4 == 0
+    pre = [f"({k_py}) % 4 == 0", f"({k_py}) > 0", f"({n_py}) > 0"]
+    tmaps = []
+    for (buf, base), (c0, pitch, apre) in zip(rs_list, affs):
         pre += apre + [f"({py_expr(c0)}) % 4 == 0", f"({py_expr(pitch)}) % 4 == 0", f"({py_expr(pitch)}) > 0"]
-        tmaps.append({"kind": "tma2d", "buf": buf, "offset": py_expr(c0), "dims": [py_expr(loop.bound), py_expr(nrows)],
-                      "pitch": py_expr(pitch), "box": [32, rows_py], "swizzle": 3})
+        pitch_py = f"(({py_expr(pitch)}) // {s_py})" if split else py_expr(pitch)
+        tmaps.append({"kind": "tma2d", "buf": buf, "offset": py_expr(c0), "dims": [kv_py, nv_py],
+                      "pitch": pitch_py, "box": [32, rows_py], "swizzle": 3})
     for buf, base in sh_list:
         pre.append(f"({py_expr(base)}) % 4 == 0")
     pre = list(dict.fromkeys(pre))
@@ -121,15 +178,20 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
     nbox = KT // 32
     # stages stay 1024-byte aligned (128B swizzle)
     boxrows_py = f"(-(-({rows_py}) // 8) * 8)"
-    stage_py = f"(-(-({len(rs_list) * nbox * 32} * {boxrows_py} + {len(sh_list) * KT}) // 256) * 256)"
+    sh_py = f"{len(sh_list) * xs} * {s_py}" if split else f"{len(sh_list) * KT}"
+    stage_py = f"(-(-({len(rs_list) * nbox * 32} * {boxrows_py} + {sh_py}) // 256) * 256)"
     # one stage (+ the 1024-byte alignment slack and the barriers) must fit the
     # 227 KiB opt-in shared memory; wider programs take the generic kernel
     pre.append(f"{stage_py} * 4 + 1024 + 64 <= 227 * 1024")
-    # ring depth: up to STAGES, as many as fit two blocks per SM for the block's rows
-    # (at least one: a one-stage ring issues each stage just before it waits on it)
-    budget = 113 * 1024
-    stages_py = (f"({STAGES} if {budget} // ({stage_py} * 4) >= {STAGES} else "
-                 f"(1 if {budget} // ({stage_py} * 4) < 1 else {budget} // ({stage_py} * 4)))")
+    # ring depth: up to STAGES (auto: MAX_STAGES), as many as the block's
+    # budget holds — half the SM's shared memory when there are two blocks
+    # per SM, all of it when the blocks fit one per SM (at least one stage:
+    # a one-stage ring issues each stage just before it waits on it)
+    cap = STAGES or MAX_STAGES
+    nblk_py = f"(-(-({nv_py}) // {rows_py}))"
+    budget_py = f"({220 * 1024} if {nblk_py} <= {SM_COUNT} else {113 * 1024})"
+    stages_py = (f"({cap} if {budget_py} // ({stage_py} * 4) >= {cap} else "
+                 f"(1 if {budget_py} // ({stage_py} * 4) < 1 else {budget_py} // ({stage_py} * 4)))")
     extra = [f"const __grid_constant__ rs_tmap rs_map{k}" for k in range(len(rs_list))]
     peer_out = int(getattr(prog, "peer_out", 0) or 0)
     if peer_out:
@@ -142,16 +204,29 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
         extra += ["const unsigned long long* __restrict__ rs_ytab", "const unsigned long long* __restrict__ rs_xtab",
                   "unsigned long long* __restrict__ rs_ticket"]
     lines = kernel_head(prog, name, temps, launch_bounds=32, extra_params=extra)
+    if split:
+        lines += [
+            f"  // a row = RS_S contiguous column chunks folded by RS_S adjacent lanes (virtual rows of K / RS_S)",
+            f"  constexpr int RS_S = {s_c}, RS_XS = {xs};",
+            f"  constexpr int RS_NROWS = {r(nrows)} * RS_S;",
+            f"  constexpr int RS_K = {r(loop.bound)} / RS_S;",
+        ]
+    else:
+        lines += [
+            f"  constexpr int RS_NROWS = {r(nrows)};",
+            f"  constexpr int RS_K = {r(loop.bound)};",
+        ]
+    sh_c = f"{len(sh_list)} * RS_S * RS_XS" if split else f"{len(sh_list) * KT}"
     lines += [
-        f"  constexpr int RS_NROWS = {r(nrows)};",
         f"  constexpr int RS_ROWS = {rows_c}, RS_KT = {KT}, RS_NBOX = {nbox};",
         "  constexpr unsigned RS_MASK = RS_ROWS == 32 ? 0xffffffffu : (1u << RS_ROWS) - 1u;",
         "  constexpr int RS_BR = (RS_ROWS + 7) / 8 * 8;  // a box's rows in shared memory (1024-byte swizzle atoms)",
-        f"  constexpr int RS_K = {r(loop.bound)};",
         "  constexpr int RS_NT = (RS_K + RS_KT - 1) / RS_KT;",
-        f"  constexpr int RS_STAGE_FLOATS = ({len(rs_list) * nbox * 32} * RS_BR + {len(sh_list) * KT} + 255) / 256 * 256;",
-        f"  constexpr int RS_FIT = {budget} / (RS_STAGE_FLOATS * 4);  // stages two blocks per SM can hold",
-        f"  constexpr int RS_STAGES = RS_FIT >= {STAGES} ? {STAGES} : (RS_FIT < 1 ? 1 : RS_FIT);",
+        f"  constexpr int RS_STAGE_FLOATS = ({len(rs_list) * nbox * 32} * RS_BR + {sh_c} + 255) / 256 * 256;",
+        "  constexpr int RS_NBLK = (RS_NROWS + RS_ROWS - 1) / RS_ROWS;",
+        f"  constexpr int RS_BUDGET = RS_NBLK <= {SM_COUNT} ? {220 * 1024} : {113 * 1024};  // one / two blocks per SM",
+        "  constexpr int RS_FIT = RS_BUDGET / (RS_STAGE_FLOATS * 4);  // stages the block's budget holds",
+        f"  constexpr int RS_STAGES = RS_FIT >= {cap} ? {cap} : (RS_FIT < 1 ? 1 : RS_FIT);",
         "  extern __shared__ __align__(1024) unsigned char rs_smem_raw[];",
         "  float* rs_smem = reinterpret_cast<float*>(rs_smem_raw + ((1024u - (rs_smem_addr(rs_smem_raw) & 1023u)) & 1023u));",
         "  unsigned long long* rs_bar = reinterpret_cast<unsigned long long*>(rs_smem + RS_STAGES * RS_STAGE_FLOATS);",
@@ -160,6 +235,9 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
         "  const bool rs_active = rs_row0 + rs_lane < RS_NROWS;",
         "  const int rs_f = rs_active ? rs_row0 + rs_lane : RS_NROWS - 1;",
     ]
+    if split:
+        lines[-1] = "  const int rs_f = (rs_active ? rs_row0 + rs_lane : RS_NROWS - 1) / RS_S;  // the real row"
+        lines.append("  const int rs_xo = (rs_lane % RS_S) * RS_XS;  // this lane's chunk of the shared streams")
     rest = "rs_f"
     for k, (var, _b) in enumerate(loops):
         if k == len(loops) - 1:
@@ -195,7 +273,7 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
         "    rs_fence_proxy_async();",
         "    if (rs_lane == 0) {",
         f"      rs_mbar_arrive_expect_tx(&rs_bar[rs_slot], (unsigned)(rs_nb * 128 * RS_ROWS * {len(rs_list)}"
-        f" + rs_kt * 4 * {len(sh_list)}));",
+        f" + rs_kt * 4 * {len(sh_list)}{' * RS_S' if split else ''}));",
     ]
     for k in range(len(rs_list)):
         lines += [
@@ -204,8 +282,16 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
             " &rs_bar[rs_slot]);",
         ]
     for k in range(len(sh_list)):
-        off = f"{len(rs_list)} * RS_NBOX * 32 * RS_BR + {k} * RS_KT"
-        lines.append(f"      rs_bulk_g2s(rs_st + {off}, rs_gx{k} + rs_j0, (unsigned)rs_kt * 4u, &rs_bar[rs_slot]);")
+        if split:
+            off = f"{len(rs_list)} * RS_NBOX * 32 * RS_BR + {k} * RS_S * RS_XS"
+            lines += [
+                "      for (int rs_c = 0; rs_c < RS_S; ++rs_c)  // chunk c of the shared stream",
+                f"        rs_bulk_g2s(rs_st + {off} + rs_c * RS_XS, rs_gx{k} + rs_c * RS_K + rs_j0, (unsigned)rs_kt * 4u,"
+                " &rs_bar[rs_slot]);",
+            ]
+        else:
+            off = f"{len(rs_list)} * RS_NBOX * 32 * RS_BR + {k} * RS_KT"
+            lines.append(f"      rs_bulk_g2s(rs_st + {off}, rs_gx{k} + rs_j0, (unsigned)rs_kt * 4u, &rs_bar[rs_slot]);")
     lines += [
         "    }",
         "  };",
@@ -213,7 +299,12 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
     ]
     vr = ValueRenderer(prog, exact)
     lines.append(f"  {acc.ctype} {acc.name};")
-    lines.append(f"  {acc.name} = {vr(init.value)};")
+    if split:  # chunks after the first start from the identity of the sum
+        lines.append(f"  {acc.name} = rs_lane % RS_S == 0 ? ({vr(init.value)}) : ({acc.ctype})0;")
+    else:
+        lines.append(f"  {acc.name} = {vr(init.value)};")
+    xoff = " + rs_xo" if split else ""
+    xstride = "RS_S * RS_XS" if split else "RS_KT"
 
     def step_with(comp):
         def hook(ld):
@@ -236,10 +327,45 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
                 f"{p}const float4 rs_a{k} = *reinterpret_cast<const float4*>(rs_st + ({k} * RS_NBOX + rs_box) * 32 * RS_BR"
                 f" + rs_lane * 32 + rs_chunk * 4);")
         for k in range(len(sh_list)):
-            off = f"{len(rs_list)} * RS_NBOX * 32 * RS_BR + {k} * RS_KT"
+            off = f"{len(rs_list)} * RS_NBOX * 32 * RS_BR + {k} * {xstride}{xoff}"
             out.append(f"{p}const float4 rs_x{k} = *reinterpret_cast<const float4*>(rs_st + {off} + rs_jj);")
         for comp in ("x", "y", "z", "w"):
             out.append(f"{p}{acc.name} = {step_with(comp)};")
+        return out
+
+    def chunk_pf(ind):
+        """A full stage's fold with the shared-memory reads PF chunks ahead
+        of their use (a register ring): the fold is one dependent add per
+        column, so with one warp per SM sub-partition an LDS issued just
+        before its use (~30 cycles) would stall every chunk."""
+        p = " " * ind
+        names = [f"rs_a{k}" for k in range(len(rs_list))] + [f"rs_x{k}" for k in range(len(sh_list))]
+
+        def loads(slot, jj):
+            out = [
+                f"{p}  const int rs_box = ({jj}) >> 5;",
+                f"{p}  const int rs_chunk = ((({jj}) >> 2) & 7) ^ rs_sw;",
+            ]
+            for k in range(len(rs_list)):
+                out.append(f"{p}  rs_pa{k}[{slot}] = *reinterpret_cast<const float4*>(rs_st + ({k} * RS_NBOX + rs_box)"
+                           " * 32 * RS_BR + rs_lane * 32 + rs_chunk * 4);")
+            for k in range(len(sh_list)):
+                off = f"{len(rs_list)} * RS_NBOX * 32 * RS_BR + {k} * {xstride}{xoff}"
+                out.append(f"{p}  rs_px{k}[{slot}] = *reinterpret_cast<const float4*>(rs_st + {off} + ({jj}));")
+            return out
+
+        out = [f"{p}float4 " + ", ".join(f"rs_p{n[3]}{n[4:]}[{PF}]" for n in names) + ";"]
+        out += [f"{p}#pragma unroll", f"{p}for (int rs_d = 0; rs_d < {PF}; ++rs_d) {{"]
+        out += loads("rs_d", "4 * rs_d")
+        out += [f"{p}}}", f"{p}#pragma unroll", f"{p}for (int rs_jj = 0; rs_jj < RS_KT; rs_jj += 4) {{",
+                f"{p}  const int rs_c = (rs_jj >> 2) % {PF};"]
+        out += [f"{p}  const float4 {n} = rs_p{n[3]}{n[4:]}[rs_c];" for n in names]
+        out += [f"{p}  if (rs_jj + {4 * PF} < RS_KT) {{"]
+        out += ["  " + x for x in loads("rs_c", f"rs_jj + {4 * PF}")]
+        out += [f"{p}  }}"]
+        for comp in ("x", "y", "z", "w"):
+            out.append(f"{p}  {acc.name} = {step_with(comp)};")
+        out += [f"{p}}}"]
         return out
 
     lines += [
@@ -250,12 +376,14 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
         "    rs_mbar_wait(&rs_bar[rs_slot], (unsigned)((rs_t / RS_STAGES) & 1));",
         "    const int rs_kt = RS_K - rs_t * RS_KT < RS_KT ? RS_K - rs_t * RS_KT : RS_KT;",
         "    if (rs_kt == RS_KT) {",
-        "#pragma unroll",
-        "      for (int rs_jj = 0; rs_jj < RS_KT; rs_jj += 4) {",
     ]
-    lines += chunk(8)
+    if PF:
+        lines += chunk_pf(6)
+    else:
+        lines += ["#pragma unroll", "      for (int rs_jj = 0; rs_jj < RS_KT; rs_jj += 4) {"]
+        lines += chunk(8)
+        lines += ["      }"]
     lines += [
-        "      }",
         "    } else {",
         "      for (int rs_jj = 0; rs_jj < rs_kt; rs_jj += 4) {",
     ]
@@ -265,8 +393,25 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
         "    }",
         "    __syncwarp(RS_MASK);",
         "  }",
-        "  if (rs_active) {",
     ]
+    if split:
+        add = "__fadd_rn" if (exact and acc.ctype == "float") else ""
+        lines += [
+            "  if (RS_S > 1) {",
+            "    // the RS_S chunk partials of a row sit in RS_S adjacent lanes: the first adds",
+            "    // the others to its own in chunk order",
+            "    const int rs_g = rs_lane & ~(RS_S - 1);",
+            f"    {acc.ctype} rs_tot = {acc.name};",
+            "#pragma unroll",
+            "    for (int rs_c = 1; rs_c < RS_S; ++rs_c)",
+            (f"      rs_tot = {add}(rs_tot, __shfl_sync(RS_MASK, {acc.name}, rs_g + rs_c));" if add else
+             f"      rs_tot = rs_tot + __shfl_sync(RS_MASK, {acc.name}, rs_g + rs_c);"),
+            f"    {acc.name} = rs_tot;",
+            "  }",
+            "  if (rs_active && rs_lane % RS_S == 0) {",
+        ]
+    else:
+        lines.append("  if (rs_active) {")
     from .emit_cuda import GenericKernel, Stage
 
     for s in post:
@@ -318,6 +463,11 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
         "order": "preserved",
         "extra_args": tmaps,
     }
+    if split:
+        plan["rows"] = nv_py
+        plan["split"] = s_py
+        plan["order"] = (f"preserved when split == 1 (rows >= {SPLIT_TARGET}, K < {SPLIT_MIN_K} or strided rows); "
+                         "else `split` contiguous column chunks per row, partials added in chunk order")
     if peer_out:
         ws_t = f"rs_ws_{name}_ticket"
         plan.update(peer_out=peer_out, workspace=[{"name": ws_t, "ctype": "int", "size": "2"}])

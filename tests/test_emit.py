@@ -313,3 +313,24 @@ def test_peer_ranks_marks_the_peer_source_inputs():
     c = compile_program(programs.NBODY_SHARD, None, name="nbodyShard")
     plan = emit_cuda(c.unit, peer_ranks=2).plan
     assert {i["name"] for i in plan["inputs"] if i.get("peer")} == {"pos", "mass"}
+
+
+@pytest.mark.parametrize("n,m,S", [(8192, 8192, 1), (4096, 8192, 2), (2048, 8192, 4), (1024, 8192, 8),
+                                   (100, 8192, 32), (1024, 1024, 1), (1024, 2048 + 4, 1)])
+def test_rowfold_split_factor(n, m, S):
+    """rowfold splits rows into column chunks only for short row counts of
+    long rows (K >= 2048, K % 128 == 0): the full-size gemv keeps the
+    program's own order."""
+    from paper_2201_03611_b200.emit_cuda import eval_py
+
+    st = _code("gemv").plan["stages"][0]
+    assert eval_py(st["split"], {"n": n, "m": m}) == S
+    assert eval_py(st["rows"], {"n": n, "m": m}) == n * S
+    rb = eval_py(str(st["row_block"]), {"n": n, "m": m})
+    assert rb % S == 0 and rb <= 32
+
+
+def test_rowfold_split_needs_reassociation():
+    c = programs.compile_config("gemv")
+    assert "split" not in emit_cuda(c.unit, reassociate=False).plan["stages"][0]
+    assert "split" in emit_cuda(c.unit).plan["stages"][0]

@@ -50,6 +50,34 @@ def test_mv_generic_kernel_bit_exact(gpu, key):
     np.testing.assert_array_equal(out, oracle.mv(M, x))
 
 
+@pytest.mark.parametrize("n,m", [(1024, 8192), (4096, 8192), (300, 8192), (5, 2048), (2000, 4096)])
+def test_mv_split_rows_within_bound(gpu, n, m):
+    """Short row counts with long rows (strong-scaled gemv bands): rowfold
+    folds each row as S contiguous column chunks in adjacent lanes and adds
+    the partials in chunk order — within the reassociated bound of every
+    row, deterministic, and bit-exact again under reassociate=False."""
+    from paper_2201_03611_b200.emit_cuda import eval_py
+
+    c = _mv(programs.MV_GLOBAL_STRATEGY)
+    code = emit_cuda(c.unit)
+    st = code.plan["stages"][0]
+    assert st["kind"] == "rowfold"
+    S = eval_py(st["split"], {"n": n, "m": m})
+    assert S > 1 and n * S >= min(8192, 32 * n) and m % (4 * S) == 0
+    M = oracle.rng_inputs(12, n, m)
+    x = oracle.rng_inputs(13, m)
+    got = run_cuda(code, c.unit, {"n": n, "m": m}, [M, x], as_numpy=True)
+    terms = M.astype(np.float64) * x.astype(np.float64)
+    y64, abs_sum = terms.sum(axis=1), np.abs(terms).sum(axis=1)
+    bound = (m // S + S + 2) * oracle.U * abs_sum + 1e-30
+    assert np.all(np.abs(got.astype(np.float64) - y64) <= bound)
+    again = run_cuda(code, c.unit, {"n": n, "m": m}, [M, x], as_numpy=True)
+    np.testing.assert_array_equal(got, again)
+    exact = emit_cuda(c.unit, reassociate=False)
+    assert "split" not in exact.plan["stages"][0]
+    np.testing.assert_array_equal(run_cuda(exact, c.unit, {"n": n, "m": m}, [M, x], as_numpy=True), oracle.mv(M, x))
+
+
 def test_mv_known_answer(gpu):
     # test_interpreter.py:37-40: M = [[1,2,3],[4,5,6]], x = [1,1,1] -> [6, 15]
     c = _mv(programs.MV_GLOBAL_STRATEGY)

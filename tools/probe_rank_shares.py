@@ -31,7 +31,7 @@ import numpy as np  # noqa: E402
 import bench  # noqa: E402
 
 
-def time_share(wl, steps):
+def time_share(wl, steps, flush=False):
     import torch
 
     from paper_2201_03611_b200 import emit_cuda
@@ -45,7 +45,7 @@ def time_share(wl, steps):
     out = torch.empty(exe.output_size, dtype=torch.float32, device="cuda")
     set_bytes = 4 * (sum(t.numel() for t in dev_in) + out.numel())
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if wl.bound == "hbm":
+    if wl.bound == "hbm" and not flush:
         n_sets = max(2, -(-bench.ROTATE_BYTES // set_bytes))
         sets = [(dev_in, out)] + [([t.clone() for t in dev_in], torch.empty_like(out)) for _ in range(n_sets - 1)]
         bound = [bench._bound_launch(exe, d, o, stream) for d, o in sets]
@@ -83,8 +83,20 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--configs", default="dot,gemv,conv,sgemm_tiled,nbody")
+    ap.add_argument("--rows", default="", help="instead: time the config at these row counts (n) on one rank")
+    ap.add_argument("--flush", action="store_true", help="every step timed alone after an L2 flush")
     args = ap.parse_args()
     import torch
+
+    if args.rows:
+        for key in args.configs.split(","):
+            cls = bench.WORKLOADS[key]
+            for n in (int(v) for v in args.rows.split(",")):
+                wl = type(f"{cls.__name__}N", (cls,), {"n": n})(rank=0, world=1, scaling="strong")
+                ms, kinds, nats = time_share(wl, args.steps, args.flush)
+                print(f"{key:12s} n={n:6d} {','.join(kinds):14s} {ms:9.4f} ms  {wl.total_work() / (ms * 1e-3) / 1e9:10.1f} "
+                      f"{wl.metric_unit}", flush=True)
+        return
 
     print(f"# {torch.cuda.get_device_name(0)}; one rank's share of each strong-scaled config (exchange excluded)")
     print("config       N  rank-0 sizes                     kernels        ms/step   aggregate if exchange free")

@@ -47,10 +47,7 @@ def patched(code):
     assert st["kind"] == "stencil2d"
     m = re.search(r"convKernel_stencil\((.*?)\) \{", text)
     text = text[:m.end(1)] + ", unsigned long long* rs_tl" + text[m.end(1):]
-    loop = "  for (int rs_t = blockIdx.x; rs_t < RS_NTILES; rs_t += gridDim.x, ++rs_it) {\n"
-    if loop not in text:  # the dynamic schedule (tiles claimed from a counter)
-        loop = "  for (int rs_it = 0;; ++rs_it) {\n"
-    assert loop in text
+    loop = re.search(r"^  for \(int rs_(t|it) = .*\{\n", text, re.M).group(0)
     text = text.replace(loop, f"  {rec(0)}\n" + loop, 1)
     top = "    const int rs_s = rs_it % RS_NSTAGE;\n"
     text = text.replace(top, top + f"    if (rs_it < {MAXIT}) {rec('1 + 2 * rs_it')}\n", 1)

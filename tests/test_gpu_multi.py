@@ -375,6 +375,7 @@ def _peer_y_worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2201_03611_b200 import emit_cuda, programs, shard
+        from paper_2201_03611_b200.emit_cuda import eval_py
         from paper_2201_03611_b200.run import Executable
 
         torch.cuda.set_device(0)
@@ -397,6 +398,34 @@ def _peer_y_worker(rank, world, port, q):
                        and np.array_equal(y.cpu().numpy(), want[r0:r0 + rows]))
             dist.barrier()  # every rank has read its full y before the next launch overwrites it
         kinds = exe.template_kinds
+        dist.barrier()
+        po.close()
+        # long rows (m >= 2048) on short bands: rowfold splits each row into
+        # column chunks — the in-kernel all-gather carries the split rows:
+        # every rank's full y equals the ranks' own (peer-free) band results
+        # gathered in rank order, within the reassociated bound
+        m = 4096
+        M = oracle.rng_inputs(3, n, m)
+        x = oracle.rng_inputs(30, m)
+        band = torch.from_numpy(np.ascontiguousarray(M[r0:r0 + rows]).reshape(-1)).cuda()
+        exe = Executable(emit_cuda(programs.compile_config("gemv").unit, peer_out=world), {"n": rows, "m": m})
+        plain = Executable(emit_cuda(programs.compile_config("gemv").unit), {"n": rows, "m": m})
+        full.zero_()
+        torch.cuda.synchronize()
+        po = shard.PeerOutput(full, r0)
+        dist.barrier()
+        exe(band, torch.from_numpy(x).cuda(), extra=po.extra)
+        torch.cuda.synchronize()
+        dist.barrier()
+        mine = plain(band, torch.from_numpy(x).cuda()).cpu().numpy()
+        parts = [None] * world
+        dist.all_gather_object(parts, mine)
+        got = full.cpu().numpy()
+        terms = M.astype(np.float64) * x.astype(np.float64)
+        S = eval_py(exe.plan["stages"][0]["split"], {"n": rows, "m": m})
+        bound = (m // S + S + 2) * oracle.U * np.abs(terms).sum(axis=1)
+        oks.append(S > 1 and np.array_equal(got, np.concatenate(parts))
+                   and bool(np.all(np.abs(got - terms.sum(axis=1)) <= bound)))
         dist.barrier()
         po.close()
         q.put((rank, oks, kinds))

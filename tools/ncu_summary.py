@@ -30,6 +30,9 @@ KEYS = [
     "smsp__warp_issue_stalled_lg_throttle_per_warp_active.pct",
     "smsp__warp_issue_stalled_not_selected_per_warp_active.pct",
     "smsp__warp_issue_stalled_selected_per_warp_active.pct",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
 ]
 SCALE = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "us": 1e-6, "ms": 1e-3, "ns": 1e-9,
          "usecond": 1e-6, "msecond": 1e-3, "nsecond": 1e-9}

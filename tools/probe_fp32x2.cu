@@ -33,6 +33,15 @@ __global__ void __launch_bounds__(512, 1) k(float* out, float s) {
         a[c] = __ffma2_rn(a[c], b[c], a[c]);
         b[c].x = __int_as_float(__float_as_int(b[c].x) ^ (i & 1));
       }
+      if (MODE == 11) {  // one packed FFMA2 and one independent scalar FFMA per chain step
+        a[c] = __ffma2_rn(a[c], b[c], a[c]);
+        b[c].x = fmaf(b[c].x, x, b[c].y);
+      }
+      if (MODE == 12) {  // one packed FFMA2 and two independent scalar FFMAs per chain step
+        a[c] = __ffma2_rn(a[c], b[c], a[c]);
+        b[c].x = fmaf(b[c].x, x, 0.5f);
+        b[c].y = fmaf(b[c].y, x, 0.25f);
+      }
       if (MODE == 5 || MODE == 6 || MODE == 7 || MODE == 9) {
         // the nbody pair body for two targets (12 packed FP32 ops): a = target
         // position component, b = accumulator; x, m = source scalars
@@ -97,5 +106,7 @@ int main() {
   run<8>("MUFU.RSQ only (2 per chain)", 2, 1);
   run<9>("nbody body, 2 ALU ops for the MUFU", 24, 1);
   run<10>("FFMA2 + LOP3 (FFMA2 lanes only)", 2, 1);
+  run<11>("FFMA2 + scalar FFMA (3 lanes per chain)", 3, 1);
+  run<12>("FFMA2 + 2 scalar FFMA (4 per chain)", 4, 1);
   return 0;
 }

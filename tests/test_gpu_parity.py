@@ -50,7 +50,8 @@ def test_mv_generic_kernel_bit_exact(gpu, key):
     np.testing.assert_array_equal(out, oracle.mv(M, x))
 
 
-@pytest.mark.parametrize("n,m", [(1024, 8192), (4096, 8192), (300, 8192), (5, 2048), (2000, 4096)])
+@pytest.mark.parametrize("n,m", [(1024, 8192), (4096, 8192), (300, 8192), (5, 2048), (2000, 4096), (8191, 2048),
+                                 (1, 8192), (2047, 2176)])
 def test_mv_split_rows_within_bound(gpu, n, m):
     """Short row counts with long rows (strong-scaled gemv bands): rowfold
     folds each row as S contiguous column chunks in adjacent lanes and adds
@@ -76,6 +77,25 @@ def test_mv_split_rows_within_bound(gpu, n, m):
     exact = emit_cuda(c.unit, reassociate=False)
     assert "split" not in exact.plan["stages"][0]
     np.testing.assert_array_equal(run_cuda(exact, c.unit, {"n": n, "m": m}, [M, x], as_numpy=True), oracle.mv(M, x))
+
+
+@pytest.mark.parametrize("n,m,s", [(256, 4096, 32), (96, 8192, 32)])
+def test_mv_opt_split_rows_within_bound(gpu, n, m, s):
+    """The paper's mv_opt schedule (work-groups of s rows) on short, long
+    matrices: the same split rows through the collapsed (wg, l) row index."""
+    from paper_2201_03611_b200.emit_cuda import eval_py
+
+    c = _mv(programs.MV_OPT_STRATEGY)
+    code = emit_cuda(c.unit)
+    nats = {"n": n, "m": m, "s": s}
+    S = eval_py(code.plan["stages"][0]["split"], nats)
+    assert S > 1
+    M = oracle.rng_inputs(14, n, m)
+    x = oracle.rng_inputs(15, m)
+    got = run_cuda(code, c.unit, nats, [M, x], as_numpy=True)
+    terms = M.astype(np.float64) * x.astype(np.float64)
+    bound = (m // S + S + 2) * oracle.U * np.abs(terms).sum(axis=1) + 1e-30
+    assert np.all(np.abs(got.astype(np.float64) - terms.sum(axis=1)) <= bound)
 
 
 def test_mv_known_answer(gpu):

@@ -439,6 +439,7 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
             "  if (rs_lane == 0) {",
             "    const unsigned long long rs_t = atomicAdd(rs_ticket, 1ull);",
             "    if (rs_t % gridDim.x == gridDim.x - 1) {",
+            "      __threadfence_system();  // acquire side: every block's fenced stores precede the publish",
             "      const unsigned rs_e = (unsigned)(rs_t / gridDim.x) + 1u;",
             f"      constexpr int RS_R = {peer_out};",
             "      const int rs_me = (int)rs_xtab[RS_R];",

@@ -10,6 +10,17 @@
 constexpr int CH = 8;      // independent chains per thread
 constexpr int IT = 4096;   // iterations
 
+__device__ __forceinline__ float ex2_approx(float v) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ float lg2_approx(float v) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(512, 1) k(float* out, float s) {
   float2 a[CH], b[CH];
@@ -41,6 +52,23 @@ __global__ void __launch_bounds__(512, 1) k(float* out, float s) {
         a[c] = __ffma2_rn(a[c], b[c], a[c]);
         b[c].x = fmaf(b[c].x, x, 0.5f);
         b[c].y = fmaf(b[c].y, x, 0.25f);
+      }
+      if (MODE == 13) { a[c].x = ex2_approx(a[c].x); a[c].y = ex2_approx(a[c].y); }  // MUFU.EX2 only
+      if (MODE == 14) { a[c].x = lg2_approx(a[c].x); a[c].y = lg2_approx(a[c].y); }  // MUFU.LG2 only
+      if (MODE == 15) {
+        // the pair body with s = m r^-3 as ex2(log2 m - 1.5 log2 r2): one FFMA2 and
+        // 2 + 2 MUFU (LG2, EX2) in place of 3 FMUL2 and 2 MUFU.RSQ
+        float2 d = __fadd2_rn(make_float2(x, x), make_float2(-a[c].x, -a[c].y));
+        float2 r2 = __ffma2_rn(d, d, make_float2(0.01f, 0.01f));
+        r2 = __ffma2_rn(d, d, r2);
+        r2 = __ffma2_rn(d, d, r2);
+        float2 l = make_float2(lg2_approx(r2.x), lg2_approx(r2.y));
+        l = __ffma2_rn(l, make_float2(-1.5f, -1.5f), m);
+        float2 q2 = make_float2(ex2_approx(l.x), ex2_approx(l.y));
+        b[c] = __ffma2_rn(d, q2, b[c]);
+        b[c] = __ffma2_rn(d, q2, b[c]);
+        b[c] = __ffma2_rn(d, q2, b[c]);
+        a[c].x += 1e-7f;
       }
       if (MODE == 5 || MODE == 6 || MODE == 7 || MODE == 9) {
         // the nbody pair body for two targets (12 packed FP32 ops): a = target
@@ -108,5 +136,8 @@ int main() {
   run<10>("FFMA2 + LOP3 (FFMA2 lanes only)", 2, 1);
   run<11>("FFMA2 + scalar FFMA (3 lanes per chain)", 3, 1);
   run<12>("FFMA2 + 2 scalar FFMA (4 per chain)", 4, 1);
+  run<13>("MUFU.EX2 only (2 per chain)", 2, 1);
+  run<14>("MUFU.LG2 only (2 per chain)", 2, 1);
+  run<15>("nbody body via LG2/EX2 (24 per chain)", 24, 1);
   return 0;
 }

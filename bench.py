@@ -619,6 +619,12 @@ class Ctx:
             self.dist.destroy_process_group()
 
 
+def _cubin_cache_dir():
+    from paper_2201_03611_b200.runtime import cache_dir
+
+    return cache_dir()
+
+
 def measure(ctx, wl, args, steps, warmup, cpu=True):
     """One config on this rank: emit, compile, time K steps (max over ranks),
     e2e through host buffers, roofline, CPU baseline (rank 0, N = 1)."""
@@ -629,8 +635,13 @@ def measure(ctx, wl, args, steps, warmup, cpu=True):
 
     rank, world, dist = ctx.rank, ctx.world, ctx.dist
     compiled, nats, host = wl.local()
+    t_emit = time.perf_counter()
     code = emit_cuda(compiled.unit, **wl.emit_kwargs)
-    exe = Executable(code, nats, device=ctx.device)
+    t_load = time.perf_counter()
+    exe = Executable(code, nats, device=ctx.device)  # NVRTC (or the on-disk cubin cache) + module load
+    t_done = time.perf_counter()
+    build_times = {"emit_s": round(t_load - t_emit, 4), "nvrtc_and_load_s": round(t_done - t_load, 4),
+                   "cubin_cache": "on (disk)" if _cubin_cache_dir() is not None else "off"}
     stream = torch.cuda.Stream()
     dev_in = [torch.from_numpy(np.ascontiguousarray(h).reshape(-1)).to("cuda") for h in host]
     out = torch.empty(exe.output_size, dtype=torch.float32, device="cuda")
@@ -826,6 +837,8 @@ def measure(ctx, wl, args, steps, warmup, cpu=True):
                 "kernels": exe.kernel_names,
                 "templates": exe.template_kinds,
                 "l2": l2_text,
+                "build": dict(build_times, note="outside every timed region (the compile is cached per process "
+                                                "and on disk, keyed by the kernel text)"),
                 "launch": ("the K timed steps captured in one CUDA graph (one kernel node per stage per step, "
                            "each step on its own input set), replayed once" if step_graph is not None else
                            "one CUDA graph per step (Executable.graph)" if use_graph else "direct rs_launch per kernel"),

@@ -1,10 +1,11 @@
 #!/usr/bin/env python3
-"""SM clock while the tensor-core GEMM runs back to back (no flush between
-launches): NVML samples every millisecond during 200 launches of the C4
-kernel, next to the achieved rate — separates the kernel's efficiency from
-the power-limited clock.  Probe only.
+"""SM clock while the tensor-core GEMM runs: back to back (b2b), with the
+bench's L2 flush before each launch (flush), or after 20 ms of idle (idle,
+the clock recovered): NVML samples every millisecond next to the achieved
+rate — separates the kernel's efficiency from the power-limited clock.
+Probe only.
 
-  python tools/probe_gemm_clock.py [--iters 200]
+  python tools/probe_gemm_clock.py [--iters 200] [--mode b2b|flush|idle]
 """
 import argparse
 import json
@@ -23,6 +24,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=200)
     ap.add_argument("--workload", default="sgemm_tiled")
+    ap.add_argument("--mode", choices=["b2b", "flush", "idle"], default="b2b",
+                    help="b2b: launches back to back; flush: the bench's L2 flush before each launch "
+                         "(outside its events); idle: 20 ms of idle before each launch")
     args = ap.parse_args()
     import pynvml
     import torch
@@ -55,18 +59,38 @@ def main():
 
     t = threading.Thread(target=sample, daemon=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush = torch.empty(bench.L2_FLUSH_BYTES // 4, device="cuda")
+    sweep = torch.ones(bench.L2_FLUSH_BYTES // 4, device="cuda")
+    per = []
     t.start()
-    e0.record(stream)
-    for _ in range(args.iters):
-        launch()
-    e1.record(stream)
-    torch.cuda.synchronize()
+    if args.mode == "b2b":
+        e0.record(stream)
+        for _ in range(args.iters):
+            launch()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.iters
+    else:
+        for _ in range(args.iters):
+            with torch.cuda.stream(stream):
+                if args.mode == "flush":
+                    flush.fill_(1.0)
+                    sweep.sum()
+            if args.mode == "idle":
+                torch.cuda.synchronize()
+                time.sleep(0.02)
+            e0.record(stream)
+            launch()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            per.append(e0.elapsed_time(e1))
+        ms = float(np.median(per))
     stop.set()
     t.join()
-    ms = e0.elapsed_time(e1) / args.iters
     clk = [c for c, _p in samples]
     pw = [p for _c, p in samples]
-    print(json.dumps({"workload": args.workload, "ms_per_launch": round(ms, 4),
+    print(json.dumps({"workload": args.workload, "mode": args.mode, "ms_per_launch": round(ms, 4),
+                      **({"ms_min": round(min(per), 4), "ms_max": round(max(per), 4)} if per else {}),
                       "tflops": round(wl.work() / (ms * 1e-3) / 1e12, 1),
                       "sm_mhz_median": float(np.median(clk)), "sm_mhz_min": min(clk), "sm_mhz_max": max(clk),
                       "power_w_median": round(float(np.median(pw)), 1), "samples": len(samples)}))

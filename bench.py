@@ -890,7 +890,41 @@ def cpu_baseline(wl, host):
         t = min(_time_once(fn) for _ in range(reps))
         out["alt"] = {"value": wl.work() / t / 1e9, "unit": wl.metric_unit, "cores": cores,
                       "kind": _cpu_kind(what), "sample": f"{what}; best of {reps}"}
+    secondary = python_reference(wl)
+    if secondary is not None:
+        out["secondary"] = secondary
     return out
+
+
+# SURVEY.md §8 d, secondary CPU baseline: the reference's pure-Python
+# functional evaluator (risec.interpreter.eval_program, interpreter.py:238;
+# ~15 us per element-op on one core), at reduced sizes so it finishes in
+# about a second per config (full size would take minutes to hours)
+PY_REF_SIZES = {"dot": {"n": 1 << 14}, "gemv": {"n": 128, "m": 128}, "conv": {"n": 64, "m": 64},
+                "sgemm_tiled": {"n": 32, "m": 32, "k": 64}, "nbody": {"n": 64}}
+
+
+def python_reference(wl):
+    """eval_program over the high-level program of `wl` at PY_REF_SIZES, one
+    execution on one core; None when the config has no reduced size."""
+    sizes = PY_REF_SIZES.get(wl.key)
+    if sizes is None or os.environ.get("RISE_BENCH_PY_REF", "1") != "1":
+        return None
+    from paper_2201_03611_b200._ref import interpreter
+
+    small = type(wl)()
+    for k, v in sizes.items():
+        setattr(small, k, v)
+    compiled, nats = small.compile()
+    inputs = [h.tolist() for h in small.global_inputs()]
+    t0 = time.perf_counter()
+    interpreter.eval_program(compiled.source_typed, nats, inputs)
+    t = time.perf_counter() - t0
+    shape = "x".join(str(v) for v in sizes.values())
+    return {"value": round(small.work() / t / 1e9, 6), "unit": wl.metric_unit, "cores": 1, "kind": "reference",
+            "sample": f"the reference's pure-Python eval_program (interpreter.py:238) on the config's RISE program at "
+                      f"{shape} (reduced: SURVEY.md §8 d secondary baseline), one execution",
+            "seconds": round(t, 3)}
 
 
 def _cpu_kind(what):

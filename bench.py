@@ -768,10 +768,15 @@ def measure(ctx, wl, args, steps, warmup, cpu=True):
         torch.cuda.synchronize()
         ctx.barrier()
         torch.cuda.synchronize()
+    step_stats = None
     if rotate:
         total_ms = float(e0.elapsed_time(e1))
     else:
-        total_ms = float(sum(starts[s_].elapsed_time(ends[s_]) for s_ in range(steps)))
+        per_step = [float(starts[s_].elapsed_time(ends[s_])) for s_ in range(steps)]
+        total_ms = float(sum(per_step))
+        step_stats = {"median": round(float(np.median(per_step)), 6), "best": round(min(per_step), 6),
+                      "worst": round(max(per_step), 6), "note": "this rank's individually timed steps (events "
+                                                                  "around each, L2 flushed before each)"}
     ms = ctx.max_over_ranks(total_ms) / steps
     total_work = wl.total_work()
     value = total_work / (ms * 1e-3) / 1e9
@@ -837,6 +842,7 @@ def measure(ctx, wl, args, steps, warmup, cpu=True):
                 "kernels": exe.kernel_names,
                 "templates": exe.template_kinds,
                 "l2": l2_text,
+                **({"step_ms": step_stats} if step_stats is not None else {}),
                 "build": dict(build_times, note="outside every timed region (the compile is cached per process "
                                                 "and on disk, keyed by the kernel text)"),
                 "launch": ("the K timed steps captured in one CUDA graph (one kernel node per stage per step, "

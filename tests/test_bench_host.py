@@ -105,3 +105,16 @@ def test_each_workload_compiles_its_own_program():
     for key, unit in want.items():
         compiled, _nats = bench.WORKLOADS[key](0, 1).compile()
         assert compiled.unit.name == unit, key
+
+
+def test_secondary_baseline_is_the_reference_interpreter():
+    """cpu_baseline.secondary (SURVEY §8 d): the reference's pure-Python
+    eval_program on each config's program at its reduced size — finishes in
+    seconds, one core, a positive rate in the config's unit."""
+    bench = _bench()
+    for key in bench.PER_CONFIG:
+        wl = bench.WORKLOADS[key]()
+        sec = bench.python_reference(wl)
+        assert sec["cores"] == 1 and sec["kind"] == "reference" and sec["unit"] == wl.metric_unit
+        assert sec["value"] > 0 and sec["seconds"] < 30
+        assert "eval_program" in sec["sample"]

@@ -138,6 +138,11 @@ int rs_event_destroy(void* event);
 int rs_event_record(void* event, void* stream);
 int rs_event_synchronize(void* event);
 int rs_event_elapsed_ms(float* ms, void* start, void* end);
+/* Work enqueued on `stream` after this call waits for `event`'s last record
+ * (cross-stream ordering without a host sync; Executable uses it to keep an
+ * executable's stateful workspaces — launch counters, exchange slots — in
+ * launch order when one executable is launched on several streams). */
+int rs_stream_wait_event(void* stream, void* event);
 
 /* ---- CUDA graphs (launch-bound multi-kernel steps) --------------------
  * Capture everything enqueued on `stream` between begin and end (e.g. every

@@ -69,6 +69,7 @@ struct Driver {
   CUresult (*EventRecord)(CUevent, CUstream);
   CUresult (*EventSynchronize)(CUevent);
   CUresult (*EventElapsedTime)(float*, CUevent, CUevent);
+  CUresult (*StreamWaitEvent)(CUstream, CUevent, unsigned);
   CUresult (*TensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -133,6 +134,7 @@ int load_driver() {
   ok &= sym(g_drv.EventRecord, "cuEventRecord");
   ok &= sym(g_drv.EventSynchronize, "cuEventSynchronize");
   ok &= sym(g_drv.EventElapsedTime, "cuEventElapsedTime");
+  ok &= sym(g_drv.StreamWaitEvent, "cuStreamWaitEvent");
   ok &= sym(g_drv.TensorMapEncodeTiled, "cuTensorMapEncodeTiled");
   ok &= sym(g_drv.GetErrorString, "cuGetErrorString");
   ok &= sym(g_drv.StreamBeginCapture, "cuStreamBeginCapture_v2");
@@ -567,6 +569,12 @@ int rs_event_destroy(void* event) {
 int rs_event_record(void* event, void* stream) {
   if (int e = ensure_ctx()) return e;
   CU(g_drv.EventRecord((CUevent)event, (CUstream)stream), "cuEventRecord");
+  return 0;
+}
+
+int rs_stream_wait_event(void* stream, void* event) {
+  if (int e = ensure_ctx()) return e;
+  CU(g_drv.StreamWaitEvent((CUstream)stream, (CUevent)event, 0), "cuStreamWaitEvent");
   return 0;
 }
 

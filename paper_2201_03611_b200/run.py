@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
 
 import numpy as np
 
@@ -93,6 +94,15 @@ class Executable:
         self._fallbacks = {}
         self._targs = targs
         self._temps = None
+        # an executable with temporaries or workspaces (launch counters, partial
+        # slots, K-split flags) carries state from one launch to the next:
+        # launch() keeps its launches in order across streams (SURVEY §8 b:
+        # thread-safe per stream) — a launch on a stream other than the last
+        # one's waits for the last one (device-side, no host sync)
+        self._stateful = bool(self.plan["temps"]) or any(st.get("workspace") for st, *_ in self.kernels)
+        self._order_lock = threading.Lock()
+        self._order_event = None
+        self._last_stream = None
 
     def _fallback(self, k):
         """Stage k's generic kernel (None for a stage without one)."""
@@ -191,11 +201,26 @@ class Executable:
                 base_args.append(ctypes.c_float(float(v)) if scalar_types[name] == "float" else ctypes.c_int(int(v)))
             else:
                 base_args.append(ctypes.c_void_p(_dptr(buffers[name])))
+        stages = []
         for st, fn, grid, block, smem, cluster in self._stages_for(buffers):
             args = list(base_args)
             for extra in st.get("extra_args", []):
                 args.append(self._extra_arg(extra, buffers, temps))
-            fn.launch(grid, block, args, smem=smem, stream=stream, cluster=cluster, flags=_launch_flags(st))
+            stages.append((st, fn, grid, block, smem, cluster, args))
+        if not self._stateful:
+            for st, fn, grid, block, smem, cluster, args in stages:
+                fn.launch(grid, block, args, smem=smem, stream=stream, cluster=cluster, flags=_launch_flags(st))
+            return
+        key = rt.stream_key(stream)
+        with self._order_lock:
+            if self._order_event is None:
+                self._order_event = rt.Event()
+            elif key != self._last_stream:
+                self._order_event.wait_on(stream)  # the previous launch on another stream first
+            for st, fn, grid, block, smem, cluster, args in stages:
+                fn.launch(grid, block, args, smem=smem, stream=stream, cluster=cluster, flags=_launch_flags(st))
+            self._order_event.record(stream)
+            self._last_stream = key
 
     def bind(self, buffers: dict, stream=None):
         """Pre-build every launch (argument arrays, tensor maps) for fixed

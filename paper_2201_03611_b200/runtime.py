@@ -33,7 +33,7 @@ EXPORTED = (
     "rs_memcpy_dtoh", "rs_memcpy_dtod", "rs_memcpy_peer", "rs_memset_d8", "rs_stream_create",
     "rs_stream_destroy", "rs_stream_synchronize", "rs_device_synchronize", "rs_event_create",
     "rs_event_destroy", "rs_event_record", "rs_event_synchronize", "rs_event_elapsed_ms",
-    "rs_tma_desc_2d_f32", "rs_ipc_handle", "rs_ipc_open", "rs_ipc_close", "rs_halo_exchange",
+    "rs_stream_wait_event", "rs_tma_desc_2d_f32", "rs_ipc_handle", "rs_ipc_open", "rs_ipc_close", "rs_halo_exchange",
     "rs_comm_unique_id", "rs_comm_init", "rs_comm_destroy", "rs_allgather",
     "rs_graph_capture_begin", "rs_graph_capture_end", "rs_graph_launch", "rs_graph_upload", "rs_graph_destroy",
 )
@@ -89,6 +89,7 @@ def lib():
             L.rs_event_record.argtypes = [vp, vp]
             L.rs_event_synchronize.argtypes = [vp]
             L.rs_event_elapsed_ms.argtypes = [ctypes.POINTER(ctypes.c_float), vp, vp]
+            L.rs_stream_wait_event.argtypes = [vp, vp]
             L.rs_tma_desc_2d_f32.argtypes = [vp, vp, ctypes.c_uint64, ctypes.c_uint64,
                                              ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, i]
             L.rs_device_attribute.argtypes = [i, ctypes.POINTER(i)]
@@ -329,6 +330,12 @@ def _dim3(d):
     return d + (1,) * (3 - len(d))
 
 
+def stream_key(stream):
+    """A hashable identity of a stream argument (None: the legacy default stream)."""
+    p = _stream_ptr(stream)
+    return None if p is None else (p.value if isinstance(p, ctypes.c_void_p) else int(p))
+
+
 def _stream_ptr(stream):
     if stream is None:
         return None
@@ -414,6 +421,10 @@ class Event:
 
     def synchronize(self):
         check_run(lib().rs_event_synchronize(self.h), "event sync")
+
+    def wait_on(self, stream=None):
+        """Make work enqueued on `stream` from now on wait for this event."""
+        check_run(lib().rs_stream_wait_event(_stream_ptr(stream), self.h), "stream wait event")
 
     def elapsed_ms(self, end: "Event") -> float:
         v = ctypes.c_float()

@@ -191,3 +191,61 @@ def test_misaligned_views_take_the_generic_kernel(gpu):
     got = exe(torch.from_numpy(a[1:].copy()).cuda(), torch.from_numpy(b).cuda(), out=out[1:])
     torch.cuda.synchronize()
     assert got.cpu().numpy()[0] == oracle.dot(a[1:], b)
+
+
+def test_concurrent_executables_on_their_own_streams(gpu):
+    """SURVEY §8 b threading: the runtime is thread-safe per stream — four
+    host threads, each with its own Executables (so their workspaces: the
+    reduce's launch counter and partial slots) on its own stream, launch a
+    dot and a gemv 25 times concurrently, plus a dot executable SHARED by all
+    four (its launches ordered across the streams by the executable); every
+    result is the single-thread result (the dot's fixed order is
+    deterministic; gemv is bit-exact)."""
+    import threading
+
+    import torch
+
+    cd, cg = _cfg("dot"), _cfg("gemv")
+    n, rows, cols = 1 << 20, 512, 1024
+    a = torch.from_numpy(oracle.rng_inputs(1, n)).cuda()
+    b = torch.from_numpy(oracle.rng_inputs(2, n)).cuda()
+    M = oracle.rng_inputs(3, rows, cols)
+    x = oracle.rng_inputs(4, cols)
+    dM, dx = torch.from_numpy(M.reshape(-1)).cuda(), torch.from_numpy(x).cuda()
+    want_dot = Executable(emit_cuda(cd.unit), {"n": n})(a, b).cpu().numpy()
+    want_mv = oracle.mv(M, x)
+    # and ONE dot executable shared by every thread: its workspaces (launch
+    # counter, partial slots) stay consistent because launch() orders an
+    # executable's launches across streams
+    shared = Executable(emit_cuda(cd.unit), {"n": n})
+    assert shared._stateful
+    torch.cuda.synchronize()
+    errors_seen = []
+
+    def worker(k):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            ed = Executable(emit_cuda(cd.unit), {"n": n})
+            eg = Executable(emit_cuda(cg.unit), {"n": rows, "m": cols})
+            outs = []
+            with torch.cuda.stream(s):
+                for _ in range(25):
+                    outs.append((ed(a, b, stream=s), eg(dM, dx, stream=s), shared(a, b, stream=s)))
+            s.synchronize()
+            for od, og, osh in outs:
+                if not (np.array_equal(od.cpu().numpy().view(np.uint32), want_dot.view(np.uint32))
+                        and np.array_equal(osh.cpu().numpy().view(np.uint32), want_dot.view(np.uint32))
+                        and np.array_equal(og.cpu().numpy(), want_mv)):
+                    errors_seen.append(k)
+                    break
+        except Exception as exc:  # noqa: BLE001 - reported below
+            errors_seen.append(f"{k}: {exc}")
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=120)
+    assert not any(t.is_alive() for t in threads)
+    assert errors_seen == []

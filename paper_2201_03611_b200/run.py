@@ -483,11 +483,15 @@ def _to_nested(arr, conv):
     return [_to_nested(a, conv) for a in arr]
 
 
-def run_cuda(code, unit, nat_assignment: dict, inputs, *, stream=None, as_numpy=False):
+def run_cuda(code, unit, nat_assignment: dict, inputs, *, stream=None, as_numpy=False, as_device=False):
     """Execute sm100a kernel text for a translated unit on the GPU and return
     its output in the interpreter's nested-value form (or a flat numpy array
-    with `as_numpy=True`).  Same contract as cexec.run_emitted (cexec.py:555):
-    inputs in unit order, sizes by name, output allocated here."""
+    with `as_numpy=True`, or the flat device tensor itself with
+    `as_device=True`: no copy back, the caller synchronises).  Same contract
+    as cexec.run_emitted (cexec.py:555): inputs in unit order, sizes by
+    name, output allocated here.  Inputs may be the reference's nested
+    values, numpy arrays, or torch tensors (a contiguous CUDA tensor of the
+    right dtype and size is used in place: the zero-copy path)."""
     import torch
 
     nat_env = {k: int(v) for k, v in dict(nat_assignment).items()}
@@ -496,12 +500,19 @@ def run_cuda(code, unit, nat_assignment: dict, inputs, *, stream=None, as_numpy=
         raise InterpreterError(f"expected {len(unit.inputs)} inputs, got {len(inputs)}")
     dev_inputs = []
     for (var, dtype), raw in zip(unit.inputs, inputs):
+        if isinstance(raw, torch.Tensor) and not isinstance(dtype, ScalarType):
+            if raw.is_cuda:
+                dev_inputs.append(raw.reshape(-1))  # Executable checks size, dtype, contiguity
+                continue
+            raw = raw.numpy()
         flat = flatten_input(raw, dtype, nat_env)
         if isinstance(dtype, ScalarType):
             dev_inputs.append(flat)
         else:
             dev_inputs.append(torch.from_numpy(np.ascontiguousarray(flat)).to("cuda"))
     out = exe(*dev_inputs, stream=stream)
+    if as_device:
+        return out
     torch.cuda.synchronize()
     host = out.cpu().numpy()
     if as_numpy:

@@ -249,3 +249,25 @@ def test_concurrent_executables_on_their_own_streams(gpu):
         t.join(timeout=120)
     assert not any(t.is_alive() for t in threads)
     assert errors_seen == []
+
+
+def test_run_cuda_device_tensors_in_and_out(gpu):
+    """run_cuda's benchmark-style use (SURVEY §8 b run entry): CUDA tensors
+    in place of nested values (zero-copy), the device output back with
+    as_device=True — the same values as the nested-list call."""
+    import torch
+
+    c = _cfg("gemv")
+    code = emit_cuda(c.unit)
+    M = oracle.rng_inputs(3, 64, 96)
+    x = oracle.rng_inputs(4, 96)
+    want = run_cuda(code, c.unit, {"n": 64, "m": 96}, [M.tolist(), x.tolist()], as_numpy=True)
+    dM, dx = torch.from_numpy(M).cuda(), torch.from_numpy(x).cuda()
+    out = run_cuda(code, c.unit, {"n": 64, "m": 96}, [dM, dx], as_device=True)
+    assert out.is_cuda and out.numel() == 64
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy(), want)
+    np.testing.assert_array_equal(run_cuda(code, c.unit, {"n": 64, "m": 96}, [dM.cpu(), dx.cpu()], as_numpy=True),
+                                  want)
+    with pytest.raises(errors.InterpreterError):
+        run_cuda(code, c.unit, {"n": 64, "m": 96}, [dM[:10], dx])

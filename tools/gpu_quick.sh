@@ -1,1 +1,2 @@
-timeout 600 python -m pytest tests -m gpu -q -x -k "concurrent or dot or capi or graph or stream_host" > gpurun_out/conc.log 2>&1; echo rc=$? >> gpurun_out/conc.log
+# quick GPU check of a test subset: K="expr" bash tools/gpu_quick.sh
+timeout 900 python -m pytest tests -m gpu -q -x -k "${K:-concurrent}" > gpurun_out/quick.log 2>&1; echo rc=$? >> gpurun_out/quick.log

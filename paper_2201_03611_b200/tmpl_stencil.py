@@ -273,18 +273,7 @@ def match(prog, stage, base_name, temps, exact, parallel_rows):
         "      // cell, which the same box holds (the box always contains an in-range row and column)",
         "      const int rs_ylo = rs_tr0 < 0 ? -rs_tr0 : 0, rs_xlo = rs_tc0 < 0 ? -rs_tc0 : 0;",
         f"      const int rs_yhi = {hdim} - rs_tr0, rs_xhi = {wdim} - rs_tc0;  // last in-range staged row / column",
-        "      // rows first (full width), then columns: corner cells end up clamped in both dimensions",
-        f"      for (int rs_e = rs_tid; rs_e < RS_SR * RS_SW; rs_e += {TX * TY}) {{",
-        "        const int rs_y = rs_e / RS_SW, rs_x = rs_e - rs_y * RS_SW;",
-        *row_pass,
-        "      }",
-        "      __syncthreads();",
-        f"      for (int rs_e = rs_tid; rs_e < RS_SR * RS_SW; rs_e += {TX * TY}) {{",
-        "        const int rs_y = rs_e / RS_SW, rs_x = rs_e - rs_y * RS_SW;",
-        "        if (rs_x < rs_xlo) rs_tile[rs_e] = rs_tile[rs_y * RS_SW + rs_xlo];",
-        "        else if (rs_x > rs_xhi) rs_tile[rs_e] = rs_tile[rs_y * RS_SW + rs_xhi];",
-        "      }",
-        "      __syncthreads();",
+    ] + _fixup_lines(row_pass, TX * TY) + [
         "    }",
         "    // this thread's register window (tile rows ty*RPT.., columns lp + tx*CPT - hcl..)",
         f"    float rs_v[{wr}][{wc}];",
@@ -454,13 +443,41 @@ def launch(st, nats, sm):
     tr, tc = st["tile"]
     tiles = -(-cols // tc) * -(-rows // tr)
     # Persistent, tile-strided: block b takes tiles b, b + G, b + 2G, ...  G is
-    # kept ≡ 2 (mod 4) and ~6 % under the resident maximum: with G a multiple
+    # kept ≡ 2 (mod 4) and ~8.5 % under the resident maximum: with G a multiple
     # of the strips per band (32 at 8192²) every block walks one column strip
     # in band steps of a power-of-two pitch and the blocks pile onto the same
-    # HBM channels — measured at 8192² with 444 slots: G = 416 0.49, 432 0.63,
-    # 440 0.73, 444 0.80, 442 0.84, 426 0.875, 418 0.878 of the copy peak.
+    # HBM channels — measured at 8192² with 444 slots (round 1): G = 416 0.49,
+    # 432 0.63, 440 0.73, 444 0.80, 442 0.84, 426 0.875, 418 0.878 of the copy
+    # peak; with the halo-only border fix-up (round 2, conv_fix_r02c.txt):
+    # 406 0.912-0.922, 410 0.89, 414 0.908, 418 0.896, 422-430 0.88.
     slots = sm * st.get("blocks_per_sm", 2)
-    grid = (int(slots * 0.94) // 4) * 4 + 2 if slots >= 8 else slots
+    grid = (int(slots * 0.913) // 4) * 4 + 2 if slots >= 8 else slots
     grid = int(os.environ.get("RISE_STENCIL_GRID", "0")) or grid  # (probe: explicit persistent grid)
     grid = max(1, min(tiles, grid))
     return (grid, 1, 1), (st["block"][0], st["block"][1], 1), st.get("smem", 0), (1, 1, 1)
+
+
+
+def _fixup_lines(row_pass, nt):
+    """The padClamp fix-up of a border tile's staged footprint, visiting only
+    the out-of-range cells: the rows outside [ylo, yhi] (full width), then
+    the columns outside [xlo, xhi] (every row), so corner cells end up
+    clamped in both dimensions.  (The round-1 form scanned the whole
+    footprint twice: strong-scaled bands 0.73 / 0.59 / 0.45 -> 0.77 / 0.67 /
+    0.57 of their N = 1 rate at 2 / 4 / 8 ranks, profiles/conv_fix_r02c.txt.)"""
+    return [
+        "      const int rs_na = rs_ylo, rs_nb = rs_yhi < RS_SR - 1 ? RS_SR - 1 - rs_yhi : 0;",
+        f"      for (int rs_q = rs_tid; rs_q < (rs_na + rs_nb) * RS_SW; rs_q += {nt}) {{",
+        "        const int rs_k = rs_q / RS_SW, rs_x = rs_q - rs_k * RS_SW;",
+        "        const int rs_y = rs_k < rs_na ? rs_k : rs_yhi + 1 + (rs_k - rs_na), rs_e = rs_y * RS_SW + rs_x;",
+        *row_pass,
+        "      }",
+        "      __syncthreads();",
+        "      const int rs_ca = rs_xlo, rs_nc = rs_ca + (rs_xhi < RS_SW - 1 ? RS_SW - 1 - rs_xhi : 0);",
+        f"      for (int rs_q = rs_tid; rs_q < RS_SR * rs_nc; rs_q += {nt}) {{",
+        "        const int rs_y = rs_q / rs_nc, rs_k = rs_q - rs_y * rs_nc;",
+        "        const int rs_x = rs_k < rs_ca ? rs_k : rs_xhi + 1 + (rs_k - rs_ca);",
+        "        rs_tile[rs_y * RS_SW + rs_x] = rs_tile[rs_y * RS_SW + (rs_k < rs_ca ? rs_xlo : rs_xhi)];",
+        "      }",
+        "      __syncthreads();",
+    ]

@@ -7,7 +7,7 @@ set -e
 cd "$(dirname "$0")/.."
 if [ "$1" = prepare ]; then
   rm -rf scratch_old; mkdir -p scratch_old/baseline
-  git archive HEAD paper_2201_03611_b200 bench.py oracle | tar -x -C scratch_old
+  git archive HEAD paper_2201_03611_b200 bench.py oracle tools | tar -x -C scratch_old
   cp -r paper_2201_03611_b200/_lib scratch_old/paper_2201_03611_b200/
   cp -r oracle/_build oracle/_ref scratch_old/oracle/ 2>/dev/null || true
   cp MEASURED_PEAKS.json scratch_old/ 2>/dev/null || true

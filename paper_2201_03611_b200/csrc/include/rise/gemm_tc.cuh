@@ -575,6 +575,7 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
 // CTA's epilogue).  Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer,
 // 2..5 hi/lo converters, 6..9 epilogue (TMEM lane quarter = warp % 4).
 constexpr int PTHREADS = 320;
+constexpr int MAX_KSPLIT = 4;  // K parts per split tile (tmpl_gemm.schedule never exceeds it)
 
 template <int M, int N, int K, int BN, int STAGES, bool B_MN = false, int GROUP_M = 0>
 RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const rs_tmap* mapA, const rs_tmap* mapB,
@@ -779,16 +780,30 @@ RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const 
                    make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
                                __uint_as_float(r[j + 3])));
         } else {
+          // the parked parts of this 32-column chunk: every load issued before the
+          // first add (one L2 round trip per chunk, not one per part and float4),
+          // then the parts added in order: deterministic.  ksplit <= MAX_KSPLIT.
+          float4 w[MAX_KSPLIT - 1][8];
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            float4 a = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                                   __uint_as_float(r[j + 3]));
-#pragma unroll 1
-            for (int p = 1; p < ksplit; ++p) {  // parts in order: deterministic
-              const float4 w = __ldcg(reinterpret_cast<const float4*>(wbase + (long long)(p - 1) * part_stride + c0 + j));
-              a = make_float4(__fadd_rn(a.x, w.x), __fadd_rn(a.y, w.y), __fadd_rn(a.z, w.z), __fadd_rn(a.w, w.w));
+          for (int p = 1; p < MAX_KSPLIT; ++p) {
+            if (p < ksplit) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                w[p - 1][j] = __ldcg(reinterpret_cast<const float4*>(wbase + (long long)(p - 1) * part_stride + c0 + 4 * j));
             }
-            store4(c0 + j, a);
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4 a = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                   __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+#pragma unroll
+            for (int p = 1; p < MAX_KSPLIT; ++p) {
+              if (p < ksplit) {
+                const float4 v = w[p - 1][j];
+                a = make_float4(__fadd_rn(a.x, v.x), __fadd_rn(a.y, v.y), __fadd_rn(a.z, v.z), __fadd_rn(a.w, v.w));
+              }
+            }
+            store4(c0 + 4 * j, a);
           }
         }
       }

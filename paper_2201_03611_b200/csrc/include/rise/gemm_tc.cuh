@@ -577,6 +577,24 @@ RS_DEVICE void gemm_3xtf32_2sm(float* __restrict__ C, int ldc, const rs_tmap* ma
 constexpr int PTHREADS = 320;
 constexpr int MAX_KSPLIT = 4;  // K parts per split tile (tmpl_gemm.schedule never exceeds it)
 
+// Probe hook (tools/probe_gemm_timeline.py; compiled out unless the probe
+// defines RS_GEMM_TIMELINE_OFFSET): %globaltimer of event e of the pair's
+// i-th unit, recorded by CTA rank 0 past the end of the workspace.
+#ifdef RS_GEMM_TIMELINE_OFFSET
+#define RS_GEMM_TL(e, i)                                                                                   \
+  do {                                                                                                     \
+    if (rank == 0 && (i) < 16) {                                                                           \
+      unsigned long long t_;                                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                              \
+      reinterpret_cast<unsigned long long*>(ws + RS_GEMM_TIMELINE_OFFSET)[((long long)pair * 16 + (i)) * 8 + (e)] = t_; \
+    }                                                                                                      \
+  } while (0)
+#else
+#define RS_GEMM_TL(e, i) \
+  do {                   \
+  } while (0)
+#endif
+
 template <int M, int N, int K, int BN, int STAGES, bool B_MN = false, int GROUP_M = 0>
 RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const rs_tmap* mapA, const rs_tmap* mapB,
                                           int n_full, int n_units, int ksplit, float* __restrict__ ws,
@@ -674,14 +692,17 @@ RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const 
         int m0, n0, kb0, kb1, khalf, sidx;
         unit_of(u, m0, n0, kb0, kb1, khalf, sidx);
         const int slot = i & 1;
+        RS_GEMM_TL(0, i);
         if (i >= 2) mbar_wait_cluster(&tmem_empty[slot], (unsigned)(((i >> 1) & 1) ^ 1));
         fence_after();
+        RS_GEMM_TL(1, i);
         const unsigned acc = tmem + (unsigned)(slot * BN);
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % STAGES;
           const unsigned ph = (unsigned)((g / STAGES) & 1);
           mbar_wait_cluster(&conv[s], ph);
           fence_after();
+          if (kb == kb0) RS_GEMM_TL(2, i);
           const unsigned long long ahi = smem_desc(rs_smem_addr(a_raw(s)));
           const unsigned long long alo = smem_desc(rs_smem_addr(a_lo(s)));
           const unsigned long long bhi =
@@ -699,6 +720,7 @@ RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const 
           commit2_multicast(&empty[s]);
         }
         commit2_multicast(&tmem_full[slot]);
+        RS_GEMM_TL(3, i);
       }
     }
     __syncwarp();
@@ -739,6 +761,7 @@ RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const 
       const int slot = i & 1;
       rs_mbar_wait(&tmem_full[slot], (unsigned)((i >> 1) & 1));
       fence_after();
+      if (t == 0) RS_GEMM_TL(4, i);
       const bool row_in = m0 + trow < M;
       float* crow = C + (long long)(row_in ? m0 + trow : 0) * ldc + n0;
       const int ncols = N - n0 < BN ? N - n0 : BN;
@@ -764,6 +787,7 @@ RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const 
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
         } while (v < (unsigned)(ksplit - 1));
       }
+      if (t == 0) RS_GEMM_TL(6, i);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         unsigned r[32];
@@ -819,6 +843,7 @@ RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const 
         }
         if (rank == 0) rs_mbar_arrive(&tmem_empty[slot]);
         else mbar_arrive_remote(mapa(rs_smem_addr(&tmem_empty[slot]), 0u));
+        RS_GEMM_TL(5, i);
       }
     }
   }

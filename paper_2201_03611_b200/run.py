@@ -101,20 +101,23 @@ class Executable:
         # one's waits for the last one (device-side, no host sync)
         self._stateful = bool(self.plan["temps"]) or any(st.get("workspace") for st, *_ in self.kernels)
         self._order_lock = threading.Lock()
+        self._temps_lock = threading.Lock()
         self._order_event = None
         self._last_stream = None
 
     def _fallback(self, k):
         """Stage k's generic kernel (None for a stage without one)."""
         if k not in self._fallbacks:
-            fb = self.launches[k][2]
-            entry = None
-            if fb is not None:
-                expr = f"{fb['name']}<{self._targs}>" if self._targs else fb["name"]
-                mod = rt.load_module(self.text, [expr], self._opts, program_name=f"{self.plan['unit']}.cu")
-                entry = (fb, mod.function(mod.lowered[0]), *self._config(fb))
-                self._fallback_modules = getattr(self, "_fallback_modules", []) + [mod]
-            self._fallbacks[k] = entry
+            with self._temps_lock:  # (compiled once even when threads race here)
+                if k not in self._fallbacks:
+                    fb = self.launches[k][2]
+                    entry = None
+                    if fb is not None:
+                        expr = f"{fb['name']}<{self._targs}>" if self._targs else fb["name"]
+                        mod = rt.load_module(self.text, [expr], self._opts, program_name=f"{self.plan['unit']}.cu")
+                        entry = (fb, mod.function(mod.lowered[0]), *self._config(fb))
+                        self._fallback_modules = getattr(self, "_fallback_modules", []) + [mod]
+                    self._fallbacks[k] = entry
         return self._fallbacks[k]
 
     # launch configuration --------------------------------------------------
@@ -151,27 +154,36 @@ class Executable:
         return [st["kind"] for st, *_ in self.kernels]
 
     def temps(self):
-        """Device temporaries (allocated once per executable)."""
+        """Device temporaries (allocated once per executable; thread-safe: the
+        table is published only once complete and its zero-fill finished)."""
         if self._temps is None:
-            import torch
-
-            # temporaries with disjoint stage lifetimes share a slot (plan "slot",
-            # emit_cuda.reuse_slots): one allocation of the largest, viewed per type
-            sizes = {}
-            for t in self.plan["temps"]:
-                k = t.get("slot", t["name"])
-                sizes[k] = max(sizes.get(k, 1), self.temp_sizes[t["name"]])
-            slots = {k: torch.empty(n, dtype=torch.float32, device="cuda") for k, n in sizes.items()}
-            self._temps = {}
-            for t in self.plan["temps"]:
-                buf = slots[t.get("slot", t["name"])][: max(1, self.temp_sizes[t["name"]])]
-                self._temps[t["name"]] = buf if t["ctype"] == "float" else buf.view(_torch_dtype(t["ctype"]))
-            for st, *_ in self.kernels:
-                for ws in st.get("workspace", []):
-                    size = eval_py(ws["size"], self.nats)
-                    self._temps[ws["name"]] = torch.zeros(max(1, size), dtype=_torch_dtype(ws["ctype"]),
-                                                          device="cuda")
+            with self._temps_lock:
+                if self._temps is None:
+                    self._temps = self._alloc_temps()
         return self._temps
+
+    def _alloc_temps(self):
+        import torch
+
+        # temporaries with disjoint stage lifetimes share a slot (plan "slot",
+        # emit_cuda.reuse_slots): one allocation of the largest, viewed per type
+        sizes = {}
+        for t in self.plan["temps"]:
+            k = t.get("slot", t["name"])
+            sizes[k] = max(sizes.get(k, 1), self.temp_sizes[t["name"]])
+        slots = {k: torch.empty(n, dtype=torch.float32, device="cuda") for k, n in sizes.items()}
+        temps = {}
+        for t in self.plan["temps"]:
+            buf = slots[t.get("slot", t["name"])][: max(1, self.temp_sizes[t["name"]])]
+            temps[t["name"]] = buf if t["ctype"] == "float" else buf.view(_torch_dtype(t["ctype"]))
+        for st, *_ in self.kernels:
+            for ws in st.get("workspace", []):
+                size = eval_py(ws["size"], self.nats)
+                temps[ws["name"]] = torch.zeros(max(1, size), dtype=_torch_dtype(ws["ctype"]), device="cuda")
+        # the workspaces' zero-fill ran on this thread's current stream; launches may
+        # come from any stream
+        torch.cuda.current_stream().synchronize()
+        return temps
 
     def _stages_for(self, buffers: dict):
         """The kernels to launch for these buffers: each template stage, or its

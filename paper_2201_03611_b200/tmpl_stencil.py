@@ -443,15 +443,17 @@ def launch(st, nats, sm):
     tr, tc = st["tile"]
     tiles = -(-cols // tc) * -(-rows // tr)
     # Persistent, tile-strided: block b takes tiles b, b + G, b + 2G, ...  G is
-    # kept ≡ 2 (mod 4) and ~8.5 % under the resident maximum: with G a multiple
+    # kept ≡ 2 (mod 4) and ~10 % under the resident maximum: with G a multiple
     # of the strips per band (32 at 8192²) every block walks one column strip
     # in band steps of a power-of-two pitch and the blocks pile onto the same
     # HBM channels — measured at 8192² with 444 slots (round 1): G = 416 0.49,
     # 432 0.63, 440 0.73, 444 0.80, 442 0.84, 426 0.875, 418 0.878 of the copy
-    # peak; with the halo-only border fix-up (round 2, conv_fix_r02c.txt):
-    # 406 0.912-0.922, 410 0.89, 414 0.908, 418 0.896, 422-430 0.88.
+    # peak; with the halo-only border fix-up and the TMA tile store (round 2,
+    # conv_fix_r02c.txt, conv_grid_r02c.txt): 382 0.925, 390 0.914, 394
+    # 0.92-0.924, 398 0.9245-0.9247, 402 0.914-0.923, 406 0.908-0.922, 410
+    # 0.89, 414 0.908, 418 0.896, 422-430 0.88.
     slots = sm * st.get("blocks_per_sm", 2)
-    grid = (int(slots * 0.913) // 4) * 4 + 2 if slots >= 8 else slots
+    grid = (int(slots * 0.895) // 4) * 4 + 2 if slots >= 8 else slots
     grid = int(os.environ.get("RISE_STENCIL_GRID", "0")) or grid  # (probe: explicit persistent grid)
     grid = max(1, min(tiles, grid))
     return (grid, 1, 1), (st["block"][0], st["block"][1], 1), st.get("smem", 0), (1, 1, 1)

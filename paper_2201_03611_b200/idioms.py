@@ -263,7 +263,10 @@ REDUCE_MINB = int(os.environ.get("RISE_REDUCE_MINB", "1"))
 # cp.async.bulk from one producer lane; the REDUCE_BLOCK folding threads only
 # read shared memory.  Order: see DESIGN.md §4.
 REDUCE_TMA = os.environ.get("RISE_REDUCE_TMA", "1") == "1"
-REDUCE_TMA_GRID = int(os.environ.get("RISE_REDUCE_TMA_GRID", "296"))
+# 256 blocks (measured at 2^24 on two boxes, profiles/dot_grid_r02c.txt:
+# 256 0.944 / 0.966 against 296 0.930 / 0.950; 128-248 and 264-512 lower):
+# 2^24 elements are 8192 chunks, exactly 32 per block
+REDUCE_TMA_GRID = int(os.environ.get("RISE_REDUCE_TMA_GRID", "256"))
 # measured (2^24, round-robin inputs, three passes on one box): 16 KiB x 3 stages
 # 0.78, 8 KiB x 4 stages 0.82 (less shared memory, more chunks in flight)
 REDUCE_TMA_CHUNK = int(os.environ.get("RISE_REDUCE_TMA_CHUNK", "8192"))

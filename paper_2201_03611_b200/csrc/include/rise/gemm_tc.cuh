@@ -643,6 +643,7 @@ RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const 
   };
 
   if (threadIdx.x == 0) {
+    if (ksplit > MAX_KSPLIT) __trap();  // the merge holds at most MAX_KSPLIT - 1 parked parts
     rs_tmap_prefetch(mapA);
     rs_tmap_prefetch(mapB);
     for (int s = 0; s < STAGES; ++s) {

@@ -11,3 +11,4 @@ timeout 900 python bench.py --impl reference > $D/ref_default.json 2> $D/ref_def
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $D/launches.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2> $D/ncu.err
 echo done >> $D/smi.txt
+timeout 900 python tools/probe_rank_shares.py > $D/rank_shares.txt 2>&1

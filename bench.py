@@ -1136,6 +1136,8 @@ def _roofline(wl, achieved, peaks, exe):
     extra = {}
     if wl.bound == "hbm":
         peak, unit, src = peaks["hbm_gbs"], "GB/s", peaks["source"]
+        extra = {"peak_note": "the measured COPY bandwidth (reads + writes); a read-only stream (gemv, dot) "
+                              "can run slightly above it (no read/write bus turnarounds)"}
     elif wl.bound == "tensor":
         # 3xTF32: three TF32 MMAs per fp32-equivalent product.  MEASURED_PEAKS
         # has no TF32 entry, so the peak is B200_PROFILING.md's dense TF32

@@ -62,22 +62,30 @@ SPLIT_TARGET = int(os.environ.get("RISE_ROWFOLD_SPLIT_TARGET", "8192"))
 SPLIT_MIN_K = int(os.environ.get("RISE_ROWFOLD_SPLIT_MIN_K", "2048"))
 
 
-def rows_per_block(nrows_py):
+def rows_per_block(nrows_py, real_rows=None):
     """Rows per block as (Python expression of the sizes, C expression of
     RS_NROWS).
 
     One lane folds one row and a block is one warp, so the rows are dealt
     out as evenly as the SMs allow: R = ceil(rows / (2 x 148)) clamped to
-    [MIN_ROWS, 32] gives two blocks on (nearly) every SM.  8192 rows -> 28
-    rows per block, 293 blocks (with 32 rows, 256 blocks leave 40 SMs one
-    block and 108 two: the two-block SMs set the time); 4096 rows -> 14;
-    1024 (a strong-scaled band at 8 GPUs) -> 4."""
+    [MIN_ROWS, 32] gives two blocks on (nearly) every SM — 4096 rows -> 14,
+    1024 (a strong-scaled band at 8 GPUs) -> 4 — except that a matrix of
+    >= 8192 real rows (`real_rows`: (python, C) expressions; not the virtual
+    rows of split rows) takes 32-row blocks: 256 blocks for 8192 rows
+    measured 0.999-1.004 of the copy peak against 0.986-0.990 for the even
+    28-row deal (293 blocks; profiles/gemv_rows_r02c.txt), while the split
+    bands keep the even deal (32-row blocks: 2-3 % slower there)."""
     if ROWS:
         return str(ROWS), str(ROWS)
     slots = 2 * SM_COUNT
     lo = MIN_ROWS
-    return (f"(32 if ({nrows_py}) > {32 * slots} else ({lo} if ({nrows_py}) <= {lo * slots} else -(-({nrows_py}) // {slots})))",
-            f"(RS_NROWS > {32 * slots} ? 32 : RS_NROWS <= {lo * slots} ? {lo} : (RS_NROWS + {slots - 1}) / {slots})")
+    py = f"(32 if ({nrows_py}) > {32 * slots} else ({lo} if ({nrows_py}) <= {lo * slots} else -(-({nrows_py}) // {slots})))"
+    c = f"(RS_NROWS > {32 * slots} ? 32 : RS_NROWS <= {lo * slots} ? {lo} : (RS_NROWS + {slots - 1}) / {slots})"
+    if real_rows is not None:
+        rpy, rc = real_rows
+        py = f"(32 if ({rpy}) >= {32 * 256} else {py})"
+        c = f"(({rc}) >= {32 * 256} ? 32 : {c})"
+    return py, c
 
 
 def affine_in_flat_row(base, loops, assumptions):
@@ -157,7 +165,7 @@ def emit(prog, loops, shape, row_streams, shared_streams, name, temps, exact, j_
         s_py = s_c = "1"
     nv_py = f"(({n_py}) * {s_py})" if split else n_py
     kv_py = f"(({k_py}) // {s_py})" if split else k_py
-    rows_py, rows_c = rows_per_block(nv_py)
+    rows_py, rows_c = rows_per_block(nv_py, (n_py, r(nrows)))
     if split:  # a row's S chunks stay in one warp, S-aligned
         rows_py = f"(-(-({rows_py}) // {s_py}) * {s_py})"
         rows_c = f"((({rows_c}) + RS_S - 1) / RS_S * RS_S)"

@@ -1,4 +1,6 @@
 #!/bin/bash
+# (historical: some knobs below belonged to experimental kernel variants that were measured and
+# removed — their patches / results are under profiles/; the script is kept as the record of the sweep)
 # conv (stencil2d): tile height (RPT rows per thread x 4) x ring depth x blocks per SM
 mkdir -p gpurun_out
 ( for cfg in "X=0" "RISE_STENCIL_TMA_STORE=0" "RISE_STENCIL_TMA_STORE=0 RISE_STENCIL_EARLY=1" "RISE_STENCIL_TMA_STORE=0 RISE_STENCIL_EARLY=1 RISE_STENCIL_RPT=4" \

@@ -1,4 +1,6 @@
 #!/bin/bash
+# (historical: some knobs below belonged to experimental kernel variants that were measured and
+# removed — their patches / results are under profiles/; the script is kept as the record of the sweep)
 # conv (stencil2d): static rounds + dynamically claimed tail rounds (RISE_STENCIL_DYN)
 mkdir -p gpurun_out
 ( RISE_STENCIL_DYN=3 timeout 600 python -m pytest tests -m gpu -q -x -k "conv or stencil or halo" 2>&1 | tail -3

@@ -1,4 +1,6 @@
 #!/bin/bash
+# (historical: some knobs below belonged to experimental kernel variants that were measured and
+# removed — their patches / results are under profiles/; the script is kept as the record of the sweep)
 mkdir -p gpurun_out
 ( for cfg in "RISE_STENCIL_SHIFT=0" "RISE_STENCIL_SHIFT=1" "RISE_STENCIL_SHIFT=37" "RISE_STENCIL_SHIFT=101" "RISE_STENCIL_SHIFT=149" \
              "RISE_STENCIL_SHIFT=222" "RISE_STENCIL_SHIFT=37 RISE_STENCIL_GRID=418" "RISE_STENCIL_SHIFT=0 RISE_STENCIL_GRID=444"; do

@@ -1,4 +1,6 @@
 mkdir -p gpurun_out
+# (historical: some knobs below belonged to experimental kernel variants that were measured and
+# removed — their patches / results are under profiles/; the script is kept as the record of the sweep)
 export STEPS=10
 bash tools/sweep.sh nbody "RISE_ALLPAIRS_PREFETCH=0" "RISE_ALLPAIRS_PREFETCH=1" "RISE_ALLPAIRS_PREFETCH=1 RISE_ALLPAIRS_FULLTILE=1" \
   "RISE_ALLPAIRS_PREFETCH=1 RISE_ALLPAIRS_UNROLL=16" "RISE_ALLPAIRS_PREFETCH=1 RISE_ALLPAIRS_JT=128" "RISE_ALLPAIRS_PREFETCH=1 RISE_ALLPAIRS_JT=32" \

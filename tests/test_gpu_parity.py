@@ -17,8 +17,10 @@ def _mv(strategy):
     return compile_program(programs.MV, strategy, name="mv")
 
 
-@pytest.mark.parametrize("n,m", [(256, 512), (100, 64), (33, 1028), (8192, 8192)])
+@pytest.mark.parametrize("n,m", [(256, 512), (100, 64), (33, 1028), (8192, 8192), (8200, 256), (16384, 516)])
 def test_mv_global_rowfold_bit_exact(gpu, n, m):
+    """(8192 rows and more take 32-row blocks: 8200 leaves a last block of 8
+    rows, 16384 x 516 a ragged last stage.)"""
     c = _mv(programs.MV_GLOBAL_STRATEGY)
     code = emit_cuda(c.unit)
     assert code.plan["stages"][0]["kind"] == "rowfold"

@@ -34,7 +34,7 @@ def test_chunked_dot_full_size(gpu):
     assert [s["kind"] for s in stages] == ["rowfold", "seqfold"]
 
 
-@pytest.mark.parametrize("n,m,s", [(2048, 1024, 32), (1000, 516, 8)])
+@pytest.mark.parametrize("n,m,s", [(2048, 1024, 32), (1000, 516, 8), (8192, 1024, 32)])
 def test_gemv_opt_schedule(gpu, n, m, s):
     cfg = programs.CONFIGS["gemv_opt"]
     c = compile_program(cfg["source"], cfg["strategy"], name="mv")

@@ -45,7 +45,13 @@ def test_bench_prints_one_contract_line_with_every_config(gpu):
     for key, entry in d["per_config"].items():
         _check_entry(entry)
         assert entry["config"]["workload"].startswith(key)
+        # build times outside the timed region; individually timed steps where the L2 is flushed
+        assert {"emit_s", "nvrtc_and_load_s"} <= set(entry["impl_detail"]["build"])
+        if key in ("sgemm_tiled", "nbody"):
+            st = entry["impl_detail"]["step_ms"]
+            assert 0 < st["best"] <= st["median"] <= st["worst"]
     assert d["per_config"]["gemv"]["value"] == d["value"]
+    assert "peak_note" in d["roofline"]  # the HBM peak is a copy rate; read-only streams may exceed it
 
 
 def test_bench_gpus_2_runs_two_ranks(gpu):

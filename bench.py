@@ -594,6 +594,8 @@ class Ctx:
             import torch.distributed as dist
 
             backend = os.environ.get("RISE_DIST_BACKEND", "nccl")  # gloo: several ranks on one GPU (testing)
+            if backend == "nccl" and world > torch.cuda.device_count():
+                backend = "gloo"  # NCCL refuses two ranks on one device (RISE_BENCH_SHARED_GPU runs)
             if backend == "nccl":
                 dist.init_process_group("nccl", device_id=torch.device("cuda", self.device))
             else:

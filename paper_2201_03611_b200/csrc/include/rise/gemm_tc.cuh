@@ -777,8 +777,64 @@ RS_DEVICE void gemm_3xtf32_2sm_persistent(float* __restrict__ C, int ldc, const 
           if (col + 3 < ncols) crow[col + 3] = v.w;
         }
       };
-      // parked parts of split tile sidx: part p (1 .. ksplit-1) at slot sidx * (ksplit-1) + p - 1
       const long long part_stride = 256LL * BN;
+      if (split && ksplit == 2) {
+        // Two K halves: each parks the column half the OTHER finalises (part 0
+        // finalises columns [0, BN/2), part 1 [BN/2, BN)), signals, waits for the
+        // other's, and adds the parked partial to its own: two half merges in
+        // parallel instead of one whole-tile merge.  Same sum either way:
+        // part0 + part1 (IEEE addition is commutative).  Flags: 4 per split tile
+        // (part x CTA rank); each part resets the flag it consumed.
+        const int own0 = khalf == 0 ? 0 : BN / 2, park0 = BN / 2 - own0;
+        float* wtile = ws + (long long)sidx * part_stride + (long long)trow * BN;
+        unsigned* myflag = flags + 4 * sidx + 2 * khalf + rank;
+        unsigned* otherflag = flags + 4 * sidx + 2 * (1 - khalf) + rank;
+#pragma unroll 1
+        for (int c0 = park0; c0 < park0 + BN / 2; c0 += 32) {
+          unsigned r[32];
+          tmem_ld32(tmem + (unsigned)(slot * BN) + ((unsigned)(q * 32) << 16) + (unsigned)c0, r);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            __stcg(reinterpret_cast<float4*>(wtile + c0 + j),
+                   make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                               __uint_as_float(r[j + 3])));
+        }
+        asm volatile("bar.sync 2, 128;" ::: "memory");  // this CTA's half is parked
+        if (t == 0) {
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");  // the parked half before the flag
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(myflag), "r"(1u) : "memory");
+        }
+        {
+          unsigned v;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(otherflag) : "memory");
+          } while (v == 0u);
+        }
+        if (t == 0) RS_GEMM_TL(6, i);
+#pragma unroll 1
+        for (int c0 = own0; c0 < own0 + BN / 2; c0 += 32) {
+          unsigned r[32];
+          tmem_ld32(tmem + (unsigned)(slot * BN) + ((unsigned)(q * 32) << 16) + (unsigned)c0, r);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {  // (independent loads: the unrolled chunk issues them together)
+            const float4 w = __ldcg(reinterpret_cast<const float4*>(wtile + c0 + 4 * j));
+            store4(c0 + 4 * j, make_float4(__fadd_rn(__uint_as_float(r[4 * j]), w.x),
+                                           __fadd_rn(__uint_as_float(r[4 * j + 1]), w.y),
+                                           __fadd_rn(__uint_as_float(r[4 * j + 2]), w.z),
+                                           __fadd_rn(__uint_as_float(r[4 * j + 3]), w.w)));
+          }
+        }
+        fence_before();
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (t == 0) {
+          *otherflag = 0u;  // consumed: ready for the next launch
+          if (rank == 0) rs_mbar_arrive(&tmem_empty[slot]);
+          else mbar_arrive_remote(mapa(rs_smem_addr(&tmem_empty[slot]), 0u));
+          RS_GEMM_TL(5, i);
+        }
+        continue;
+      }
+      // parked parts of split tile sidx: part p (1 .. ksplit-1) at slot sidx * (ksplit-1) + p - 1
       float* wbase = ws + ((long long)(split ? sidx : 0) * (ksplit - 1)) * part_stride + (long long)trow * BN;
       float* wrow = wbase + (long long)(khalf > 0 ? khalf - 1 : 0) * part_stride;
       unsigned* flag = flags + 2 * (split ? sidx : 0) + rank;

@@ -323,7 +323,7 @@ def emit(prog, desc, base_name, temps):
             ],
             # K-split tiles park their parts 1.. here: (parts - 1) x split tiles <= one wave of pair tiles
             "workspace": [{"name": f"rs_ws_{base_name}_ktail", "ctype": "float", "size": f"74 * 256 * {PAIR_BN}"},
-                          {"name": f"rs_ws_{base_name}_kflags", "ctype": "int", "size": "2 * 74"}],
+                          {"name": f"rs_ws_{base_name}_kflags", "ctype": "int", "size": "4 * 74"}],
         }
         return "\n".join(lines) + "\n", plan
     lines += [
